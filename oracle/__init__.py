@@ -1,0 +1,186 @@
+"""ctypes front-end of the CPU oracle (oracle.c) -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may import
+this package.  It never imports the CUDA product package and the product never imports it.
+Functions accept any object with the attributes of workloads.SparseMatrix holding numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(HERE, "oracle.c")
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC", "-o", LIB_PATH, src])
+    return LIB_PATH
+
+
+class _Matrix(ctypes.Structure):
+    _fields_ = [("format", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("nrows", ctypes.c_int64), ("ncols", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("nouter", ctypes.c_int64), ("outer_crd", ctypes.c_void_p), ("pos", ctypes.c_void_p),
+                ("crd", ctypes.c_void_p), ("val", ctypes.c_void_p)]
+
+
+class _Parts(ctypes.Structure):
+    _fields_ = [("P", ctypes.c_int32), ("k", ctypes.c_int32), ("query", ctypes.c_void_p),
+                ("row", ctypes.c_void_p), ("row_pos", ctypes.c_void_p), ("col", ctypes.c_void_p),
+                ("pos", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        L = _lib
+        vp = ctypes.c_void_p
+        L.oracle_validate.argtypes = [vp]
+        L.oracle_total_cost.argtypes = [ctypes.c_int32, vp]
+        L.oracle_total_cost.restype = ctypes.c_int64
+        L.oracle_queries.argtypes = [ctypes.c_int64, ctypes.c_int32, vp]
+        L.oracle_partition_rank.argtypes = [ctypes.c_int32, vp, ctypes.c_int32, vp]
+        L.oracle_partition_alg1.argtypes = [ctypes.c_int32, vp, ctypes.c_int32, vp, vp]
+        L.oracle_lb_search.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
+        L.oracle_lb_search.restype = ctypes.c_int64
+        L.oracle_spmv.argtypes = [vp, vp, vp]
+        L.oracle_spmm.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, vp, ctypes.c_int64]
+        L.oracle_spadd_k.argtypes = [ctypes.c_int32, vp, vp, vp, vp, ctypes.c_int64]
+        L.oracle_spadd_k.restype = ctypes.c_int64
+        L.oracle_spadd_counts.argtypes = [ctypes.c_int32, vp, vp, vp]
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _matrices(ops):
+    keep = []
+    arr = (_Matrix * len(ops))()
+    for i, A in enumerate(ops):
+        pos = np.ascontiguousarray(A.pos, dtype=np.int64)
+        crd = np.ascontiguousarray(A.crd, dtype=np.int32)
+        val = np.ascontiguousarray(A.val)
+        outer = None if A.outer_crd is None else np.ascontiguousarray(A.outer_crd, dtype=np.int32)
+        keep += [pos, crd, val, outer]
+        arr[i].format = 0 if A.format == "csr" else 1
+        arr[i].dtype = 1 if val.dtype == np.float64 else 0
+        arr[i].nrows, arr[i].ncols = A.nrows, A.ncols
+        arr[i].nnz = crd.shape[0]
+        arr[i].nouter = pos.shape[0] - 1
+        arr[i].outer_crd, arr[i].pos, arr[i].crd, arr[i].val = _p(outer), _p(pos), _p(crd), _p(val)
+    return arr, keep
+
+
+class Parts:
+    """Partition record (Listing 7 `Parts`): SoA arrays of length P+1."""
+
+    def __init__(self, P, k):
+        self.P, self.k = P, k
+        self.query = np.zeros(P + 1, np.int64)
+        self.row = np.zeros(P + 1, np.int64)
+        self.row_pos = np.zeros(P + 1, np.int64)
+        self.col = np.zeros(P + 1, np.int32)
+        self.pos = np.zeros((P + 1) * k, np.int64)
+
+    def c(self):
+        s = _Parts()
+        s.P, s.k = self.P, self.k
+        s.query, s.row, s.row_pos, s.col, s.pos = (_p(self.query), _p(self.row), _p(self.row_pos),
+                                                   _p(self.col), _p(self.pos))
+        return s
+
+    def pos2(self):
+        return self.pos.reshape(self.P + 1, self.k)
+
+
+def validate(A) -> int:
+    arr, keep = _matrices([A])
+    return lib().oracle_validate(ctypes.byref(arr[0]))
+
+
+def total_cost(ops) -> int:
+    arr, keep = _matrices(ops)
+    return lib().oracle_total_cost(len(ops), arr)
+
+
+def queries(qstar: int, P: int) -> np.ndarray:
+    Q = np.zeros(P + 1, np.int64)
+    lib().oracle_queries(qstar, P, _p(Q))
+    return Q
+
+
+def partition_rank(ops, P) -> Parts:
+    arr, keep = _matrices(ops)
+    out = Parts(P, len(ops))
+    s = out.c()
+    if lib().oracle_partition_rank(len(ops), arr, P, ctypes.byref(s)) != 0:
+        raise ValueError("oracle_partition_rank failed")
+    return out
+
+
+def partition_alg1(ops, P, with_probes=False):
+    arr, keep = _matrices(ops)
+    out = Parts(P, len(ops))
+    probes = np.zeros(P + 1, np.int64)
+    s = out.c()
+    if lib().oracle_partition_alg1(len(ops), arr, P, ctypes.byref(s), _p(probes)) != 0:
+        raise ValueError("oracle_partition_alg1 failed")
+    return (out, probes) if with_probes else out
+
+
+def lb_search(crd, lo, hi, x) -> int:
+    crd = np.ascontiguousarray(crd, dtype=np.int32)
+    return lib().oracle_lb_search(_p(crd) if crd.size else None, lo, hi, x)
+
+
+def spmv(A, x) -> np.ndarray:
+    arr, keep = _matrices([A])
+    x = np.ascontiguousarray(x, dtype=A.val.dtype)
+    y = np.zeros(A.pos.shape[0] - 1, dtype=A.val.dtype)
+    lib().oracle_spmv(ctypes.byref(arr[0]), _p(x), _p(y))
+    return y
+
+
+def spmm(A, B) -> np.ndarray:
+    arr, keep = _matrices([A])
+    B = np.ascontiguousarray(B, dtype=A.val.dtype)
+    nb = B.shape[1]
+    C = np.zeros((A.nrows, nb), dtype=A.val.dtype)
+    if lib().oracle_spmm(ctypes.byref(arr[0]), _p(B), nb, nb, _p(C), nb) != 0:
+        raise ValueError("oracle_spmm: CSR only")
+    return C
+
+
+def spadd_k(ops):
+    """Returns (z_pos, z_crd, z_val) of the k-way structural union with left-fold values."""
+    arr, keep = _matrices(ops)
+    cap = int(sum(int(A.crd.shape[0]) for A in ops))
+    M = ops[0].nrows
+    z_pos = np.zeros(M + 1, np.int64)
+    z_crd = np.zeros(max(cap, 1), np.int32)
+    z_val = np.zeros(max(cap, 1), dtype=ops[0].val.dtype)
+    n = lib().oracle_spadd_k(len(ops), arr, _p(z_pos), _p(z_crd), _p(z_val), cap)
+    if n < 0:
+        raise ValueError("oracle_spadd_k failed")
+    return z_pos, z_crd[:n].copy(), z_val[:n].copy()
+
+
+def spadd_counts(ops, parts: Parts) -> np.ndarray:
+    arr, keep = _matrices(ops)
+    cnt = np.zeros(parts.P, np.int64)
+    s = parts.c()
+    if lib().oracle_spadd_counts(len(ops), arr, ctypes.byref(s), _p(cnt)) != 0:
+        raise ValueError("oracle_spadd_counts failed")
+    return cnt

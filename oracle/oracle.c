@@ -1,0 +1,343 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY (see oracle.h).  Plain, slow, single-threaded.
+ *
+ * Every function follows a definition or an algorithm of the paper (PAPER.md line cited)
+ * step by step, without blocking, fusion or reordering.  Where the paper is silent the
+ * reading taken is named "R<n>" and listed in DESIGN.md ("Readings of the paper").
+ *
+ * Nothing here is shared with the CUDA path.
+ */
+#include "oracle.h"
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ helpers */
+
+static long double vget_ld(const or_matrix *A, int64_t q) {
+    return A->dtype == OR_F64 ? (long double)((const double *)A->val)[q]
+                              : (long double)((const float *)A->val)[q];
+}
+/* row coordinate of outer position ip (P:1679 CSR dense row level; P:562 DCSR compressed row level) */
+static int64_t row_of(const or_matrix *A, int64_t ip) {
+    return A->format == OR_DCSR ? (int64_t)A->outer_crd[ip] : ip;
+}
+
+/* lb_search of Listing 7: "Find least ipA in [lA, hA] s.t. A[ipA] >= i".
+ * Returns hi+1 when every crd in [lo, hi] is < x (and lo when the window is empty). */
+int64_t oracle_lb_search(const int32_t *crd, int64_t lo, int64_t hi, int64_t x) {
+    int64_t a = lo, b = hi + 1;            /* answer in [a, b] */
+    while (a < b) {
+        int64_t m = a + (b - a) / 2;
+        if ((int64_t)crd[m] >= x) b = m; else a = m + 1;
+    }
+    return a;
+}
+
+/* ------------------------------------------------------------- validation */
+/* Sorted-level invariants ("These are sorted formats") and DCSR canonical
+ * form (R10: stored rows are non-empty). */
+int oracle_validate(const or_matrix *A) {
+    if (A->nrows < 0 || A->ncols < 0 || A->nnz < 0) return 1;
+    if (A->format == OR_CSR && A->nouter != A->nrows) return 2;
+    if (A->pos[0] != 0) return 3;
+    if (A->pos[A->nouter] != A->nnz) return 4;
+    for (int64_t i = 0; i < A->nouter; i++) {
+        if (A->pos[i + 1] < A->pos[i]) return 5;
+        for (int64_t q = A->pos[i]; q < A->pos[i + 1]; q++) {
+            if (A->crd[q] < 0 || (int64_t)A->crd[q] >= A->ncols) return 6;
+            if (q > A->pos[i] && A->crd[q] <= A->crd[q - 1]) return 7;
+        }
+    }
+    if (A->format == OR_DCSR) {
+        for (int64_t i = 0; i < A->nouter; i++) {
+            if (A->outer_crd[i] < 0 || (int64_t)A->outer_crd[i] >= A->nrows) return 8;
+            if (i > 0 && A->outer_crd[i] <= A->outer_crd[i - 1]) return 9;
+            if (A->pos[i + 1] == A->pos[i]) return 10;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------- total cost and queries */
+/* Q* = sum of non-zeros of every sparse operand ("sum of the number of non-zeros
+ * contained in each sparse tensor"); dense operands cost nothing (R5). */
+int64_t oracle_total_cost(int32_t k, const or_matrix *ops) {
+    int64_t q = 0;
+    for (int32_t o = 0; o < k; o++) q += ops[o].nnz;
+    return q;
+}
+
+/* Q_p = p * Q* / P, rounded down (R4), computed in 128-bit. */
+void oracle_queries(int64_t qstar, int32_t P, int64_t *Q) {
+    for (int32_t p = 0; p <= P; p++) Q[p] = (int64_t)(((__int128)p * (__int128)qstar) / (__int128)P);
+}
+
+static void set_origin(int32_t k, or_parts *out, int32_t p) {
+    out->row[p] = 0; out->row_pos[p] = 0; out->col[p] = 0;
+    for (int32_t o = 0; o < k; o++) out->pos[(int64_t)p * k + o] = 0;
+}
+static void set_end(int32_t k, const or_matrix *ops, or_parts *out, int32_t p) {
+    out->row[p] = ops[0].nrows;
+    out->row_pos[p] = ops[0].nouter;
+    out->col[p] = 0;
+    for (int32_t o = 0; o < k; o++) out->pos[(int64_t)p * k + o] = ops[o].nnz;
+}
+/* number of stored rows of operand 0 with coordinate < row (CSR: row itself) */
+static int64_t outer_lb(const or_matrix *A, int64_t row) {
+    if (A->format == OR_CSR) return row;
+    int64_t a = 0, b = A->nouter;
+    while (a < b) { int64_t m = a + (b - a) / 2; if ((int64_t)A->outer_crd[m] >= row) b = m; else a = m + 1; }
+    return a;
+}
+
+/* --------------------------------------- partition: the plain definition (rank) */
+/*
+ * The cost of coiterating from the origin to coordinate x (Theorem 1's C(x)) with the
+ * nnz-count cost functions is the number of stored entries, over all operands, that come
+ * lexicographically before x.  The highest coordinate whose cost is <= Q is therefore the
+ * coordinate of entry number Q (0-indexed) of the lexicographically sorted multiset E of all stored
+ * entries, and the positions are the per-operand counts of entries strictly before it.
+ * One sweep enumerates E in order (the k-finger merge of Listing 1, in union form).
+ * b_0 = origin and b_P = end (R1); an interior query with Q_p >= Q* (only when Q* = 0) is the end.
+ */
+int oracle_partition_rank(int32_t k, const or_matrix *ops, int32_t P, or_parts *out) {
+    if (k < 1 || P < 1) return 1;
+    int64_t qstar = oracle_total_cost(k, ops);
+    oracle_queries(qstar, P, out->query);
+    int64_t *q  = (int64_t *)calloc((size_t)k, sizeof(int64_t));   /* cursor position per operand */
+    int64_t *ip = (int64_t *)calloc((size_t)k, sizeof(int64_t));   /* outer position per operand */
+    int64_t c = 0;                                                   /* entries enumerated so far */
+    int32_t p = 1;
+    while (p < P) {
+        int64_t best_r = -1, best_c = -1;
+        for (int32_t o = 0; o < k; o++) {
+            if (q[o] >= ops[o].nnz) continue;
+            while (ops[o].pos[ip[o] + 1] <= q[o]) ip[o]++;           /* outer position holding q[o] */
+            int64_t r = row_of(&ops[o], ip[o]), cc = ops[o].crd[q[o]];
+            if (best_r < 0 || r < best_r || (r == best_r && cc < best_c)) { best_r = r; best_c = cc; }
+        }
+        if (best_r < 0) break;                                       /* E exhausted */
+        int32_t g = 0;                                               /* entries with this coordinate */
+        for (int32_t o = 0; o < k; o++)
+            if (q[o] < ops[o].nnz && row_of(&ops[o], ip[o]) == best_r && ops[o].crd[q[o]] == best_c) g++;
+        while (p < P && out->query[p] < c + g) {                      /* E[Q_p] has this coordinate */
+            out->row[p] = best_r;
+            out->row_pos[p] = outer_lb(&ops[0], best_r);
+            out->col[p] = (int32_t)best_c;
+            for (int32_t o = 0; o < k; o++) out->pos[(int64_t)p * k + o] = q[o];
+            p++;
+        }
+        for (int32_t o = 0; o < k; o++)
+            if (q[o] < ops[o].nnz && row_of(&ops[o], ip[o]) == best_r && ops[o].crd[q[o]] == best_c) q[o]++;
+        c += g;
+    }
+    for (; p < P; p++) set_end(k, ops, out, p);
+    set_origin(k, out, 0);
+    set_end(k, ops, out, P);
+    free(q); free(ip);
+    return 0;
+}
+
+/* ------------------------------------- partition: literal Alg. 1 (Listing 7 form) */
+/*
+ * FindPartition (Alg. 1) over the loop order i -> j with the CSR cost functions of
+ * Listing 5 -- or, for a DCSR row level, the compressed-level query of P:1735-1737 --
+ * searched as in Listing 7: an outer binary search with midpoint low+(high-low+1)/2
+ * (P:1783), an inner lb_search per operand, and windows [l, h] that narrow as the search proceeds
+ * (P:1790-1793).  The window update on a rejected midpoint uses h = ip - 1 (Listing 7 writes
+ * hA = ipA, which can probe one past the window; the result is identical -- reading R15).
+ * Domains: x_i in [0, M], x_j in [0, N) (R2).  If x_i = M the boundary is the end.
+ */
+static void find_partition_alg1(int32_t k, const or_matrix *ops, int64_t Q, or_parts *out, int32_t p,
+                                int64_t *probes) {
+    int64_t n_probe = 0;
+    int64_t R = Q;
+    const int64_t M = ops[0].nrows, N = ops[0].ncols;
+    int64_t *lo = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    int64_t *hi = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    int64_t *ipv = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    int64_t *rp = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+
+    /* ---- level m = i : HighestCoordinateLeqQuery over x_i in [0, M] (Alg. 1 line 7) ---- */
+    for (int32_t o = 0; o < k; o++) {        /* outer windows (used for DCSR compressed rows) */
+        lo[o] = 0; hi[o] = ops[o].nouter - 1; rp[o] = 0;
+    }
+    int64_t low = 0, high = M, cost_low = 0;  /* C_i(0) = 0 */
+    while (low < high) {
+        int64_t x = low + (high - low + 1) / 2;
+        int64_t cost = 0;
+        for (int32_t o = 0; o < k; o++) {
+            if (ops[o].format == OR_CSR) {
+                ipv[o] = x;                                               /* dense level: position == coordinate */
+                cost += ops[o].pos[x] - ops[o].pos[0];                    /* Listing 5: C_i = A.pos[x_i] - A.pos[0] */
+            } else {
+                ipv[o] = oracle_lb_search(ops[o].outer_crd, lo[o], hi[o], x);  /* stored rows with coordinate < x */
+                cost += ops[o].pos[ipv[o]] - ops[o].pos[0];
+            }
+        }
+        n_probe++;
+        if (cost <= R) { low = x; cost_low = cost; for (int32_t o = 0; o < k; o++) { lo[o] = ipv[o]; rp[o] = ipv[o]; } }
+        else           { high = x - 1; for (int32_t o = 0; o < k; o++) hi[o] = ipv[o] - 1; }
+    }
+    int64_t xi = low;
+    R -= cost_low;                                                   /* Alg. 1 line 8 */
+    if (xi >= M) {
+        set_end(k, ops, out, p);
+    } else {
+        /* ---- level m = j : HighestCoordinateLeqQuery over x_j in [0, N) within row xi ---- */
+        int64_t *seg = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+        for (int32_t o = 0; o < k; o++) {
+            int64_t r = (ops[o].format == OR_CSR) ? xi : rp[o];     /* outer position of row xi (if stored) */
+            if (ops[o].format == OR_DCSR) {
+                /* rp[o] = #stored rows with coordinate < xi (window start after the outer search) */
+                r = oracle_lb_search(ops[o].outer_crd, 0, ops[o].nouter - 1, xi);
+            }
+            int stored = (ops[o].format == OR_CSR) || (r < ops[o].nouter && ops[o].outer_crd[r] == xi);
+            seg[o] = ops[o].pos[r];
+            lo[o] = ops[o].pos[r];
+            hi[o] = stored ? ops[o].pos[r + 1] - 1 : ops[o].pos[r] - 1;
+            rp[o] = r;
+        }
+        int64_t jlow = 0, jhigh = N - 1;
+        while (jlow < jhigh) {
+            int64_t x = jlow + (jhigh - jlow + 1) / 2;
+            int64_t cost = 0;
+            for (int32_t o = 0; o < k; o++) {
+                ipv[o] = oracle_lb_search(ops[o].crd, lo[o], hi[o], x);    /* Listing 7 line 8-10 */
+                cost += ipv[o] - seg[o];                                    /* Listing 5: C_j = x_jp - A.pos[x_i] */
+            }
+            n_probe++;
+            if (cost <= R) { jlow = x; for (int32_t o = 0; o < k; o++) lo[o] = ipv[o]; }
+            else           { jhigh = x - 1; for (int32_t o = 0; o < k; o++) hi[o] = ipv[o] - 1; }
+        }
+        out->row[p] = xi;
+        out->row_pos[p] = rp[0];
+        out->col[p] = (int32_t)jlow;
+        for (int32_t o = 0; o < k; o++) out->pos[(int64_t)p * k + o] = lo[o];   /* Listing 7 line 20: p.ipA = lA */
+        free(seg);
+    }
+    if (probes) probes[p] = n_probe;
+    free(lo); free(hi); free(ipv); free(rp);
+}
+
+int oracle_partition_alg1(int32_t k, const or_matrix *ops, int32_t P, or_parts *out, int64_t *probes) {
+    if (k < 1 || P < 1) return 1;
+    int64_t qstar = oracle_total_cost(k, ops);
+    oracle_queries(qstar, P, out->query);
+    for (int32_t p = 1; p < P; p++) find_partition_alg1(k, ops, out->query[p], out, p, probes);
+    set_origin(k, out, 0);  if (probes) probes[0] = 0;      /* R1 */
+    set_end(k, ops, out, P); if (probes) probes[P] = 0;
+    return 0;
+}
+
+/* ---------------------------------------------------------------- SpMV */
+/* y_i = sum_j A_ij x_j (the broadcast example y = A x of P:1742-1744).  Products and sums in long
+ * double (exact products for fp32 inputs), rounded once to the value type (R13). */
+int oracle_spmv(const or_matrix *A, const void *x, void *y) {
+    for (int64_t ip = 0; ip < A->nouter; ip++) {
+        long double acc = 0.0L;
+        for (int64_t q = A->pos[ip]; q < A->pos[ip + 1]; q++) {
+            long double xv = A->dtype == OR_F64 ? (long double)((const double *)x)[A->crd[q]]
+                                                : (long double)((const float *)x)[A->crd[q]];
+            acc += vget_ld(A, q) * xv;
+        }
+        if (A->dtype == OR_F64) ((double *)y)[ip] = (double)acc;
+        else                    ((float *)y)[ip]  = (float)acc;
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------- SpMM */
+/* C_ik = sum_j A_ij B_jk, loop order i -> j -> k (Listing 6 broadcast; R6). */
+int oracle_spmm(const or_matrix *A, const void *B, int64_t ldb, int32_t nb, void *C, int64_t ldc) {
+    if (A->format != OR_CSR) return 1;
+    long double *acc = (long double *)malloc(sizeof(long double) * (size_t)(nb > 0 ? nb : 1));
+    for (int64_t i = 0; i < A->nrows; i++) {
+        for (int32_t c = 0; c < nb; c++) acc[c] = 0.0L;
+        for (int64_t q = A->pos[i]; q < A->pos[i + 1]; q++) {
+            long double a = vget_ld(A, q);
+            int64_t j = A->crd[q];
+            for (int32_t c = 0; c < nb; c++) {
+                long double b = A->dtype == OR_F64 ? (long double)((const double *)B)[j * ldb + c]
+                                                   : (long double)((const float *)B)[j * ldb + c];
+                acc[c] += a * b;
+            }
+        }
+        for (int32_t c = 0; c < nb; c++) {
+            if (A->dtype == OR_F64) ((double *)C)[i * ldc + c] = (double)acc[c];
+            else                    ((float *)C)[i * ldc + c]  = (float)acc[c];
+        }
+    }
+    free(acc);
+    return 0;
+}
+
+/* -------------------------------------------------------------- k-way SpAdd */
+/*
+ * Z = A_0 + ... + A_{k-1}: coiteration over the union (Listing 2, in CSR form), one
+ * k-finger merge per row.  Structure is the structural union (TACO assembly is symbolic).
+ * Z.val(i,j) = left fold in operand order over the operands that store (i,j), starting from the
+ * first present value (R9), in the value type's own arithmetic.
+ */
+int64_t oracle_spadd_k(int32_t k, const or_matrix *ops, int64_t *z_pos, int32_t *z_crd, void *z_val,
+                       int64_t capacity) {
+    for (int32_t o = 0; o < k; o++) if (ops[o].format != OR_CSR) return -1;
+    const int64_t M = ops[0].nrows;
+    const int f64 = ops[0].dtype == OR_F64;
+    int64_t *q = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    int64_t nz = 0;
+    z_pos[0] = 0;
+    for (int64_t i = 0; i < M; i++) {
+        for (int32_t o = 0; o < k; o++) q[o] = ops[o].pos[i];
+        for (;;) {
+            int64_t j = -1;
+            for (int32_t o = 0; o < k; o++)
+                if (q[o] < ops[o].pos[i + 1] && (j < 0 || ops[o].crd[q[o]] < j)) j = ops[o].crd[q[o]];
+            if (j < 0) break;
+            double vd = 0.0; float vf = 0.0f; int have = 0;
+            for (int32_t o = 0; o < k; o++) {
+                if (q[o] < ops[o].pos[i + 1] && ops[o].crd[q[o]] == j) {
+                    if (f64) { double a = ((const double *)ops[o].val)[q[o]]; vd = have ? vd + a : a; }
+                    else     { float  a = ((const float *)ops[o].val)[q[o]];  vf = have ? vf + a : a; }
+                    have = 1;
+                    q[o]++;
+                }
+            }
+            if (nz >= capacity) { free(q); return -1; }
+            z_crd[nz] = (int32_t)j;
+            if (f64) ((double *)z_val)[nz] = vd; else ((float *)z_val)[nz] = vf;
+            nz++;
+        }
+        z_pos[i + 1] = nz;
+    }
+    free(q);
+    return nz;
+}
+
+/* Per-partition assembly counts: the number of union coordinates c with
+ * b_p <=lex c <lex b_{p+1}; matching coordinates of different operands fall in one partition
+ * because the cut is in coordinate space. */
+int oracle_spadd_counts(int32_t k, const or_matrix *ops, const or_parts *parts, int64_t *cnt) {
+    for (int32_t o = 0; o < k; o++) if (ops[o].format != OR_CSR) return 1;
+    const int32_t P = parts->P;
+    const int64_t M = ops[0].nrows;
+    int64_t *q = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    for (int32_t p = 0; p < P; p++) cnt[p] = 0;
+    int32_t p = 0;
+    for (int64_t i = 0; i < M; i++) {
+        for (int32_t o = 0; o < k; o++) q[o] = ops[o].pos[i];
+        for (;;) {
+            int64_t j = -1;
+            for (int32_t o = 0; o < k; o++)
+                if (q[o] < ops[o].pos[i + 1] && (j < 0 || ops[o].crd[q[o]] < j)) j = ops[o].crd[q[o]];
+            if (j < 0) break;
+            /* advance p while c >= b_{p+1} (lexicographic on (row, col)) */
+            while (p + 1 < P && (i > parts->row[p + 1] || (i == parts->row[p + 1] && j >= parts->col[p + 1]))) p++;
+            cnt[p]++;
+            for (int32_t o = 0; o < k; o++)
+                if (q[o] < ops[o].pos[i + 1] && ops[o].crd[q[o]] == j) q[o]++;
+        }
+    }
+    free(q);
+    return 0;
+}

@@ -1,0 +1,77 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU oracle for the data-parallel hot path of
+ * Chougule et al., "Partitioning Unstructured Sparse Tensor Algebra for
+ * Load-Balanced Parallel Execution" (arXiv 2604.17198, "Nacho").  Citations
+ * "P:<line>" refer to /root/reference/PAPER.md.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+ * load this library.  It shares no code, header, helper or constant with the
+ * CUDA path (paper_2604_17198_b200/); it defines its own types below.
+ *
+ * Conventions:
+ *   positions (pos) int64, coordinates in crd int32, row coordinates int64,
+ *   values fp32 (dtype 0) or fp64 (dtype 1).
+ */
+#ifndef NACHO_ORACLE_H
+#define NACHO_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OR_CSR  0
+#define OR_DCSR 1
+#define OR_F32  0
+#define OR_F64  1
+
+typedef struct {
+    int32_t        format;     /* OR_CSR (Dense o Compressed) or OR_DCSR (Compressed o Compressed) */
+    int32_t        dtype;      /* OR_F32 / OR_F64 */
+    int64_t        nrows, ncols, nnz;
+    int64_t        nouter;     /* CSR: nrows; DCSR: number of stored rows */
+    const int32_t *outer_crd;  /* DCSR only: [nouter] stored row coordinates, strictly increasing */
+    const int64_t *pos;        /* [nouter+1] */
+    const int32_t *crd;        /* [nnz] */
+    const void    *val;        /* [nnz] */
+} or_matrix;
+
+typedef struct {
+    int32_t  P, k;
+    int64_t *query;    /* [P+1] Q_p */
+    int64_t *row;      /* [P+1] boundary row coordinate */
+    int64_t *row_pos;  /* [P+1] outer-level position of the boundary (CSR: == row) */
+    int32_t *col;      /* [P+1] boundary column coordinate */
+    int64_t *pos;      /* [(P+1)*k] per-operand positions */
+} or_parts;
+
+/* 0 if the operand satisfies the format invariants of P:1675-1684 (sorted levels), else a code > 0 */
+int     oracle_validate(const or_matrix *A);
+int64_t oracle_total_cost(int32_t k, const or_matrix *ops);
+void    oracle_queries(int64_t qstar, int32_t P, int64_t *Q);
+
+/* Partition boundaries by the plain definition (rank of the Q-th entry of the lexicographic
+ * multiset of all stored entries).  Returns 0 on success. */
+int     oracle_partition_rank(int32_t k, const or_matrix *ops, int32_t P, or_parts *out);
+/* Partition boundaries by literal Alg. 1 in the Listing 7 form.
+ * probes[p] (optional) receives the number of cost-function evaluations for boundary p. */
+int     oracle_partition_alg1(int32_t k, const or_matrix *ops, int32_t P, or_parts *out, int64_t *probes);
+/* lb_search of Listing 7: least position in [lo, hi] with crd[pos] >= x, or hi+1. */
+int64_t oracle_lb_search(const int32_t *crd, int64_t lo, int64_t hi, int64_t x);
+
+/* y = A x.  CSR: y[nrows]; DCSR: compressed y[nouter] aligned with outer_crd.  Wide accumulation. */
+int     oracle_spmv(const or_matrix *A, const void *x, void *y);
+/* C = A B, B [ncols x nb] with leading dimension ldb, C [nrows x nb] with ldc (CSR only). */
+int     oracle_spmm(const or_matrix *A, const void *B, int64_t ldb, int32_t nb, void *C, int64_t ldc);
+/* Z = sum_o ops[o] (k-way structural union, CSR).  Z.pos[nrows+1]; z_crd/z_val need capacity >= nnz_Z.
+ * Values: left fold in operand order starting from the first present value.  Returns nnz_Z, or -1. */
+int64_t oracle_spadd_k(int32_t k, const or_matrix *ops, int64_t *z_pos, int32_t *z_crd, void *z_val, int64_t capacity);
+/* Per-partition union counts for given boundaries: cnt[p] = #union coordinates c with b_p <=lex c <lex b_{p+1}. */
+int     oracle_spadd_counts(int32_t k, const or_matrix *ops, const or_parts *parts, int64_t *cnt);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
