@@ -1,0 +1,443 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the partitioned hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nacho|reference] [--workload c2|c5]
+
+One step = one full pass of the hot path over the workload: partition (Alg. 1) +
+the partitioned kernel(s).  Default workload: BASELINE.json configs[1] = C2, the 3-operand CSR
+SpAdd A+B+C, 1M x 1M, 1e7 nnz each (a9-a11), metric GNNZ/s = Q*/time (Q* = sum of operand nnz).
+The other configurations (C5 CSR SpMV, C3 DCSR SpMV, C4 SpMM, C1 fp64 SpMV) are measured in the
+same run and reported under "kernels".  Prints ONE JSON line on rank 0.
+
+--impl reference times the CPU oracle (oracle/, single-threaded C) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="nacho", choices=["nacho", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"])
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--quick", action="store_true", help="skip the secondary configurations")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_table():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}", "--format=csv,noheader",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1].split()[0]))
+                mx = max(mx, float(r[2].split()[0]))
+                for n, v in zip(names, r[5:9]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ timing helpers
+class Timer:
+    """CUDA events on the launching stream; per-step times with an untimed L2 flush between steps."""
+
+    def __init__(self, torch, flush_bytes):
+        self.torch = torch
+        self.flush = torch.empty(flush_bytes // 4, dtype=torch.float32, device="cuda")
+
+    def flush_l2(self):
+        self.flush.zero_()
+
+    def run(self, step, K, W, sections=None, soak_s=0.0):
+        t = self.torch
+        for _ in range(W):
+            self.flush_l2()
+            step()
+        t.cuda.synchronize()
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < soak_s:   # untimed: keeps the GPU busy under the clock sampler
+            for _ in range(20):
+                self.flush_l2()
+                step()
+            t.cuda.synchronize()
+        times = []
+        sec = {}
+        for _ in range(K):
+            self.flush_l2()
+            ev = [t.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+            marks = step(timed=True) if sections else step()
+            ev[1].record()
+            times.append((ev, marks))
+        t.cuda.synchronize()
+        out = [e[0].elapsed_time(e[1]) for e, _ in times]
+        if sections:
+            for _, marks in times:
+                for i, name in enumerate(sections):
+                    sec.setdefault(name, []).append(marks[i].elapsed_time(marks[i + 1]))
+        return out, sec
+
+
+def ev(torch):
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+# ------------------------------------------------------------------ workloads
+def bench_spadd(N, W, torch, args, timer, world, rank):
+    wl = W.build("c2", args.scale, device="cuda")
+    ops = wl.ops
+    k = len(ops)
+    M = ops[0].nrows
+    nnz = [A.nnz for A in ops]
+    qstar = sum(nnz)
+    if world > 1:  # device-level cut: this rank runs partitions [rank*P_l, (rank+1)*P_l) of P_total
+        from paper_2604_17198_b200 import dist
+        P_l = N.auto_partitions(ops, "spadd") // world + 1
+        P = P_l * world
+    else:
+        P = N.auto_partitions(ops, "spadd")
+    parts = N.Parts(P, k, ops[0].pos.device)
+    local = parts if world == 1 else dist.slice_parts(parts, rank * P_l, (rank + 1) * P_l)
+    part_off = torch.empty(local.P + 1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(8 * (local.P + 64), dtype=torch.uint8, device="cuda")
+    z_pos = torch.empty(M + 1, dtype=torch.int64, device="cuda")
+    z_crd = torch.empty(qstar, dtype=torch.int32, device="cuda")   # capacity Q* >= nnz_Z (no host sync)
+    z_val = torch.empty(qstar, dtype=ops[0].val.dtype, device="cuda")
+
+    def step(timed=False):
+        m = [ev(torch)] if timed else None
+        N.partition(ops, P, out=parts)
+        if timed:
+            m.append(ev(torch))
+        N.spadd_k_count(ops, local, part_off, ws)
+        if timed:
+            m.append(ev(torch))
+        N.spadd_k_fill(ops, local, part_off, qstar, z_pos, z_crd, z_val)
+        if timed:
+            m.append(ev(torch))
+        return m
+
+    sections = ["partition", "count+scan", "fill"]
+    step()
+    torch.cuda.synchronize()
+    N.launch_count(reset=True)
+    step()
+    launches = N.launch_count(reset=True)
+    times, sec = timer.run(step, args.steps, args.warmup, sections, soak_s=1.0)
+    nnz_z = int(part_off[-1].item())
+    vs = ops[0].val.element_size()
+    algo_step = sum(n * (4 + vs) + (M + 1) * 8 for n in nnz) + nnz_z * (4 + vs) + (M + 1) * 8
+    fill_bytes = sum(n * (4 + vs) + (M + 1) * 8 for n in nnz) + nnz_z * (4 + vs) + (M + 1) * 8
+    count_bytes = sum(n * 4 + (M + 1) * 8 for n in nnz)
+    res = dict(work=qstar / world if world > 1 else qstar, times=times, sec=sec, launches=launches,
+               algo_step=algo_step, nnz_z=nnz_z, P=P,
+               kernel_bytes={"fill": fill_bytes, "count+scan": count_bytes,
+                             "partition": (P + 1) * (8 * k + 28)},
+               dtype="f32" if vs == 4 else "f64", wl=wl, parts=parts)
+    return res
+
+
+def e2e_spadd(N, torch, wl, args):
+    """Same metric through the public API with pinned host inputs; H2D + D2H inside the timed region."""
+    host = []
+    for A in wl.ops:
+        host.append([t.cpu().pin_memory() for t in (A.pos, A.crd, A.val)])
+    dev = [[torch.empty_like(t, device="cuda") for t in h] for h in host]
+    import workloads as W
+    ops = [W.SparseMatrix("csr", A.nrows, A.ncols, d[0], d[1], d[2]) for A, d in zip(wl.ops, dev)]
+    h2d = sum(t.numel() * t.element_size() for h in host for t in h)
+    P = N.auto_partitions(ops, "spadd")
+    parts = N.Parts(P, len(ops), "cuda")
+    out_host = {}
+
+    def step():
+        for h, d in zip(host, dev):
+            for a, b in zip(h, d):
+                b.copy_(a, non_blocking=True)
+        N.partition(ops, P, out=parts)
+        z_pos, z_crd, z_val = N.spadd_k(ops, parts)          # host reads nnz_Z (two-pass)
+        out_host["pos"] = z_pos.cpu()
+        out_host["crd"] = z_crd.cpu()
+        out_host["val"] = z_val.cpu()
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    K = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    e0 = ev(torch)
+    for _ in range(K):
+        step()
+    e1 = ev(torch)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    d2h = sum(t.numel() * t.element_size() for t in out_host.values())
+    qstar = sum(A.nnz for A in ops)
+    return {"value": qstar / (ms * 1e-3) / 1e9, "unit": "GNNZ/s", "ms_per_step": ms, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / K}
+
+
+def bench_spmv(N, W, torch, name, scale, K, Wu, timer, column_kind=None):
+    wl = W.build(name, scale, device="cuda", column_kind=column_kind)
+    A = wl.ops[0]
+    P = wl.P or N.auto_partitions([A], "spmv")
+    parts = N.Parts(P, 1, "cuda")
+    n_y = A.nrows if A.format == "csr" else A.nouter
+    y = torch.empty(n_y, dtype=A.val.dtype, device="cuda")
+    ws = torch.empty(N.lib.nacho_spmv_workspace_size(__import__("ctypes").byref(N.matrix(A)), P), dtype=torch.uint8,
+                     device="cuda")
+
+    def step(timed=False):
+        m = [ev(torch)] if timed else None
+        N.partition([A], P, out=parts)
+        if timed:
+            m.append(ev(torch))
+        N.spmv(A, wl.x, parts, y=y, ws=ws)
+        if timed:
+            m.append(ev(torch))
+        return m
+
+    times, sec = timer.run(step, K, Wu, ["partition", "spmv+fixup"])
+    vs = A.val.element_size()
+    M, Nc, nnz = A.nrows, A.ncols, A.nnz
+    if A.format == "csr":
+        algo = nnz * (4 + vs) + (M + 1) * 8 + M * vs + Nc * vs
+    else:
+        distinct = int(torch.unique(A.crd).numel())
+        algo = nnz * (4 + vs) + A.nouter * (4 + 8) + distinct * vs + A.nouter * vs
+    return dict(work=nnz, times=times, sec=sec, algo_step=algo, kernel_bytes={"spmv+fixup": algo}, P=P,
+                dtype="f32" if vs == 4 else "f64", wl=wl)
+
+
+def bench_spmm(N, W, torch, scale, K, Wu, timer):
+    wl = W.build("c4", scale, device="cuda")
+    A = wl.ops[0]
+    P = N.auto_partitions([A], "spmm")
+    parts = N.Parts(P, 1, "cuda")
+    C = torch.empty(A.nrows, wl.nb, dtype=A.val.dtype, device="cuda")
+
+    def step(timed=False):
+        m = [ev(torch)] if timed else None
+        N.partition([A], P, out=parts)
+        if timed:
+            m.append(ev(torch))
+        N.spmm(A, wl.x, parts, C=C)
+        if timed:
+            m.append(ev(torch))
+        return m
+
+    times, sec = timer.run(step, K, Wu, ["partition", "spmm+fixup"])
+    M, Nc, nnz, nb = A.nrows, A.ncols, A.nnz, wl.nb
+    algo = nnz * 8 + (M + 1) * 8 + Nc * nb * 4 + M * nb * 4
+    return dict(work=nnz, times=times, sec=sec, algo_step=algo, kernel_bytes={"spmm+fixup": algo}, P=P, dtype="f32",
+                wl=wl)
+
+
+def summarize(r, peak, world=1):
+    ms = statistics.mean(r["times"])
+    dom = max(r["sec"], key=lambda s: statistics.mean(r["sec"][s]))
+    dms = statistics.mean(r["sec"][dom])
+    achieved = r["kernel_bytes"][dom] / (dms * 1e-3) / 1e9
+    out = {"gnnz_s": r["work"] * world / (ms * 1e-3) / 1e9, "ms_per_step": ms,
+           "step_hbm_frac": r["algo_step"] / (ms * 1e-3) / 1e9 / peak,
+           "sections_ms": {s: statistics.mean(v) for s, v in r["sec"].items()},
+           "dominant": dom, "dominant_achieved_gbs": achieved, "P": r["P"]}
+    return out, dom, dms, achieved
+
+
+# ------------------------------------------------------------------ CPU oracle (baseline / reference arm)
+def oracle_spadd_once(O, host_ops, P):
+    t0 = time.perf_counter()
+    O.partition_rank(host_ops, P)
+    O.spadd_k(host_ops)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(host_ops, P, budget_s=20.0):
+    import oracle as O
+    O.lib()
+    qstar = sum(A.nnz for A in host_ops)
+    ts = []
+    t_start = time.perf_counter()
+    while len(ts) < 3 or (time.perf_counter() - t_start < budget_s * 0.5 and len(ts) < 14):
+        ts.append(oracle_spadd_once(O, host_ops, P))
+        if time.perf_counter() - t_start > budget_s:
+            break
+    med = statistics.median(ts)
+    return {"value": qstar / med / 1e9, "unit": "GNNZ/s", "cores": 1, "kind": "oracle",
+            "sample": f"full C2 workload (3 x {host_ops[0].nnz} nnz, P={P}): oracle partition_rank + spadd_k, "
+                      f"median of {len(ts)} runs on 1 host core, {med:.3f} s each"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    import workloads as W
+    O.lib()
+    wl = W.build("c2", args.scale)
+    host = wl.ops
+    qstar = sum(A.nnz for A in host)
+    P = -(-qstar // 2046)
+    for _ in range(args.warmup):
+        oracle_spadd_once(O, host, P)
+    ts = [oracle_spadd_once(O, host, P) for _ in range(args.steps)]
+    ms = statistics.mean(ts) * 1e3
+    v = qstar / (ms * 1e-3) / 1e9
+    line = {"impl": "reference", "metric": "GNNZ/s (3-way CSR SpAdd A+B+C, C2)", "value": v, "unit": "GNNZ/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "c2_spadd3_1Mx1M_3x1e7nnz", "scale": args.scale},
+            "cpu_baseline": {"value": v, "unit": "GNNZ/s", "cores": 1, "kind": "oracle",
+                             "sample": f"full C2 workload each step ({qstar} nnz), oracle partition_rank + spadd_k"},
+            "e2e": {"value": v, "unit": "GNNZ/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    import paper_2604_17198_b200 as N
+    import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak, peak_src = peaks()
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    timer = Timer(torch, max(2 * l2, 256 << 20))
+
+    clocks = Clocks(local)
+    r = bench_spadd(N, W, torch, args, timer, world, rank)
+    clk = clocks.stop()
+
+    times = r["times"]
+    ms_local = statistics.mean(times)
+    ms = ms_local
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms_local], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    summ, dom, dms, achieved = summarize(r, peak)
+    tt = traffic_table().get(f"c2:{dom}")
+    line = {
+        "metric": "GNNZ/s (3-way CSR SpAdd A+B+C: partition + count/scan + fill), % of HBM roofline",
+        "value": sum(A.nnz for A in r["wl"].ops) / (ms * 1e-3) / 1e9,
+        "unit": "GNNZ/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": r["dtype"], "data": "synthetic (seeded power-law CSR, workloads/ recipe)",
+        "config": {"workload": "c2_spadd3_1Mx1M_3x1e7nnz", "k": 3, "nnz_per_operand": r["wl"].ops[0].nnz,
+                   "nnz_Z": r["nnz_z"], "P": r["P"], "scale": args.scale,
+                   "l2": "flushed between timed steps (untimed memset of 2x L2)", "parallelism": f"dp{world}"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": tt, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": r["kernel_bytes"][dom]},
+        "step_roofline_frac": summ["step_hbm_frac"],
+        "sections_ms": summ["sections_ms"],
+        "gpu_launches": r["launches"] * args.steps,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_e2e:
+        line["e2e"] = e2e_spadd(N, torch, r["wl"], args)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        host = [A.numpy() for A in r["wl"].ops]
+        line["cpu_baseline"] = cpu_baseline(host, r["P"])
+    wl_keep = r.pop("wl")
+    del wl_keep, r
+    torch.cuda.empty_cache()
+    if not args.quick and world == 1:
+        kern = {}
+        for name, fn in [("c5_spmv_csr_f32", lambda: bench_spmv(N, W, torch, "c5", args.scale, 10, 3, timer)),
+                         ("c3_spmv_dcsr_f32", lambda: bench_spmv(N, W, torch, "c3", args.scale, 10, 3, timer)),
+                         ("c4_spmm_f32_nb64", lambda: bench_spmm(N, W, torch, args.scale, 5, 2, timer)),
+                         ("c1_spmv_csr_f64_P8", lambda: bench_spmv(N, W, torch, "c1", 1.0, 20, 3, timer))]:
+            try:
+                rr = fn()
+                s, d, _, ach = summarize(rr, peak)
+                kern[name] = {"gnnz_s": s["gnnz_s"], "ms_per_step": s["ms_per_step"],
+                              "step_hbm_frac": s["step_hbm_frac"], "dominant": d,
+                              "dominant_hbm_frac": ach / peak, "sections_ms": s["sections_ms"], "P": s["P"],
+                              "traffic": traffic_table().get(f"{name.split('_')[0]}:{d}")}
+                del rr
+            except Exception as e:  # report, never hide
+                kern[name] = {"error": repr(e)[:300]}
+            torch.cuda.empty_cache()
+        line["kernels"] = kern
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,157 @@
+/*
+ * nacho.h -- C ABI of libnacho.so: load-balanced partitioning of sparse tensor algebra and the
+ * partitioned kernels that execute over it, on NVIDIA B200 (sm_100a).
+ *
+ * Paper: Chougule, Root, Lacouture, Yan, Yadav, Kjolstad, "Partitioning Unstructured Sparse Tensor
+ * Algebra for Load-Balanced Parallel Execution" (arXiv 2604.17198).  P:<n> = PAPER.md line n.
+ *
+ * Conventions for every entry point
+ *   - All array pointers are DEVICE pointers, borrowed: the caller allocates and owns them (e.g.
+ *     torch tensors).  Inputs are read-only during the call; outputs must not alias inputs.
+ *   - Calls are asynchronous on `stream` (a cudaStream_t passed as void*); none synchronises the host.
+ *   - The library holds no device allocations; scratch space is the caller's `ws` of at least
+ *     *_workspace_size() bytes (pass NULL/0 when the size is 0).
+ *   - Argument errors are detected on the host before any launch and return a status != 0; the
+ *     message is available from nacho_last_error() (thread-local).  Launch failures return
+ *     NACHO_ERR_CUDA.  No C++ exception crosses this ABI.
+ *   - Types (reading R11): positions int64, column coordinates int32, row coordinates int64, values
+ *     fp32 or fp64.
+ */
+#ifndef NACHO_H
+#define NACHO_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NACHO_SUCCESS = 0,
+  NACHO_ERR_INVALID_ARG = 1, /* null pointer, P < 1, k outside [1, NACHO_MAX_K], unsupported dtype/format */
+  NACHO_ERR_SHAPE = 2,       /* operand shapes disagree (k-way ops), or x / B do not match A */
+  NACHO_ERR_FORMAT = 3,      /* nacho_validate found a violated sorted-level invariant */
+  NACHO_ERR_OVERFLOW = 4,    /* ncols > INT32_MAX, or a count does not fit the index types */
+  NACHO_ERR_WORKSPACE = 5,   /* ws_bytes smaller than the *_workspace_size() result */
+  NACHO_ERR_CUDA = 6         /* a launch or CUDA runtime call failed */
+} nacho_status;
+
+typedef enum { NACHO_CSR = 0, NACHO_DCSR = 1 } nacho_format;
+typedef enum { NACHO_F32 = 0, NACHO_F64 = 1 } nacho_dtype;
+
+#define NACHO_MAX_K 8
+
+/* A sparse matrix in a TACO level format:
+ *   CSR  = Dense(rows) o Compressed(cols)       -- pos[nrows+1], crd[nnz]
+ *   DCSR = Compressed(rows) o Compressed(cols)  -- outer_crd[nouter], pos[nouter+1]
+ * pos[0] = 0, pos non-decreasing, pos[nouter] = nnz; crd strictly increasing within each row
+ * segment and < ncols; DCSR outer_crd strictly increasing and every stored row non-empty (R10). */
+typedef struct {
+  int32_t format;            /* nacho_format */
+  int32_t dtype;             /* nacho_dtype of val */
+  int64_t nrows, ncols, nnz;
+  int64_t nouter;            /* CSR: == nrows; DCSR: number of stored rows */
+  const int32_t* outer_crd;  /* DCSR: [nouter]; CSR: NULL */
+  const int64_t* pos;        /* [nouter + 1] */
+  const int32_t* crd;        /* [nnz] */
+  const void* val;           /* [nnz] */
+} nacho_matrix;
+
+/* The partition record `Parts` of Listing 7 and Listing 8 (p.i, p.jpA, p.jpB;
+ * P:2120-2126), as structure-of-arrays of P+1 boundaries.  Partition p covers the lexicographic
+ * coordinate range [b_p, b_{p+1}).  b_0 is the origin (row 0, col 0, pos 0) and b_P the end
+ * (row nrows, row_pos nouter, col 0, pos[o] = nnz_o) -- reading R1.  All arrays caller-allocated. */
+typedef struct {
+  int32_t P;         /* number of partitions (>= 1) */
+  int32_t k;         /* number of sparse operands coiterated */
+  int64_t* query;    /* [P+1]  Q_p = floor(p * Q* / P)                                (R4) */
+  int64_t* row;      /* [P+1]  boundary row coordinate x_i                             (Alg. 1) */
+  int64_t* row_pos;  /* [P+1]  outer-level position of x_i (CSR: == row; DCSR: index into outer_crd) */
+  int32_t* col;      /* [P+1]  boundary column coordinate x_j                          (Alg. 1) */
+  int64_t* pos;      /* [(P+1)*k] pos[p*k+o] = #entries of operand o before b_p        (P:1795 p.ipA) */
+} nacho_parts;
+
+/* ------------------------------------------------------------------------------------------------
+ * nacho_partition -- Alg. 1 "FindPartition" run for every boundary p = 0..P with the
+ * query Q_p = floor(p*Q* /P), Q* = sum_o nnz_o, using the CSR / DCSR
+ * cost functions of Listing 5 and the position-space specialisation of Listing 7
+ * (P:1752-1799).  One warp per boundary performs a 32-ary search over the row level and, for k > 1,
+ * a k-way order-statistic search over the row's column segments (matching coordinates of different
+ * operands always land on the same side of a cut).  Result: the unique highest
+ * coordinate with cost <= Q_p (Theorem 1: 0 <= Q_p - C(b_p) < k).
+ *   ops   host array of k operand descriptors (device arrays inside); all must share format, nrows
+ *         and ncols.  DCSR requires k == 1.
+ *   out   caller-allocated device arrays for P+1 boundaries; out->P and out->k must equal P and k.
+ * Errors: INVALID_ARG (k, P, nulls, DCSR with k > 1), SHAPE (mismatched operands), OVERFLOW. */
+nacho_status nacho_partition(const nacho_matrix* ops, int32_t k, int32_t P, nacho_parts* out, void* stream);
+
+/* Partition count the kernels below pick when the caller does not fix P: ceil(Q* / tile), tile being
+ * the per-CTA work of the kernel for that operation (op: 0 spmv, 1 spadd, 2 spmm). */
+int32_t nacho_auto_partitions(const nacho_matrix* ops, int32_t k, int32_t op);
+
+/* ------------------------------------------------------------------------------------------------
+ * nacho_spmv -- y = A x over a partition of A (SpMV is the broadcast example of P:1742-1744; the
+ * per-partition loop bounds follow Listing 8).  Partition p streams the positions
+ * [parts.pos[p], parts.pos[p+1]); rows finished inside p are written by p (ownership rule R7: p
+ * owns rows [b_p.row, b_{p+1}.row - 1], empty rows are written as 0); a row cut by a boundary
+ * leaves a carry that a fix-up kernel adds in partition order.
+ *   A       CSR or DCSR, fp32 or fp64.
+ *   parts   a partition of A with k == 1 (from nacho_partition), or NULL: the library then computes
+ *           one with nacho_auto_partitions(A, 1, 0) partitions inside `ws`.
+ *   x       [ncols] dense, dtype of A.
+ *   y       CSR: [nrows].  DCSR: [nouter] compressed y aligned with outer_crd (R12), or [nrows]
+ *           when dense_y != 0 (then rows not stored are written as 0).
+ *   ws      >= nacho_spmv_workspace_size(A, parts ? parts->P : 0) bytes (carries [+ parts]).
+ * Numerics: products and sums in the value type; summation order differs from the sequential one
+ * (R13), so results agree with the oracle to 1e-5 (fp32) / 1e-12 (fp64) relative to sum|a*x|. */
+size_t nacho_spmv_workspace_size(const nacho_matrix* A, int32_t P);
+nacho_status nacho_spmv(const nacho_matrix* A, const nacho_parts* parts, const void* x, void* y, int32_t dense_y,
+                        void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * k-way SpAdd Z = A_0 + ... + A_{k-1} (CSR, union coiteration of Listing 2), assembled in
+ * the paper's two passes (Fig. 7a):
+ *   nacho_spadd_k_count : per partition, symbolic k-way union merge -> cnt_p; exclusive prefix sum
+ *                         -> part_off[0..P] with part_off[P] = nnz_Z.
+ *   (caller reads part_off[P], allocates z_crd / z_val of nnz_Z entries -- the one host sync)
+ *   nacho_spadd_k_fill  : re-merge, write (col, value) at part_off[p] and the Z.pos entries of the
+ *                         rows partition p owns (guarded single writer, R7).
+ * Z.pos[0] = 0.  Values: left fold in operand order of the present values (R9), in the value type --
+ * bit-identical to the oracle.  Structural zeros are kept (symbolic assembly).
+ *   ops      k CSR operands of identical shape and dtype.   parts: k-operand partition of ops.
+ *   part_off [P+1] int64 (device).   z_pos [nrows+1] int64.   z_crd [nnz_Z] int32, z_val [nnz_Z].
+ *   ws       >= nacho_spadd_k_workspace_size(ops, k, P). */
+size_t nacho_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P);
+nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
+                                 void* ws, size_t ws_bytes, void* stream);
+nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_parts* parts,
+                                const int64_t* part_off, int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws,
+                                size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * nacho_spmm -- C = A B with loop order i -> j -> k (Listing 6): A is broadcast over k,
+ * whose cost factor N_k is uniform, so the cuts are A's one-operand cuts and k is never cut (R6).
+ *   A      CSR, fp32 or fp64.       parts: k == 1 partition of A, or NULL (auto, inside ws).
+ *   B      [ncols x nb] row-major with leading dimension ldb >= nb.   C: [nrows x nb], ldc >= nb.
+ *   nb     1..256 (64 is the tuned case).
+ *   ws     >= nacho_spmm_workspace_size(A, P, nb). */
+size_t nacho_spmm_workspace_size(const nacho_matrix* A, int32_t P, int32_t nb);
+nacho_status nacho_spmm(const nacho_matrix* A, const nacho_parts* parts, const void* B, int64_t ldb, int32_t nb,
+                        void* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.
+ * Synchronous on `stream` (it reads one flag back).  Returns NACHO_ERR_FORMAT on a violation. */
+nacho_status nacho_validate(const nacho_matrix* A, void* stream);
+
+/* Message for the last non-success status on this thread ("" if none). */
+const char* nacho_last_error(void);
+
+/* Number of kernel launches issued by this library on this thread since the last reset (for the
+ * benchmark's gpu_launches claim). */
+int64_t nacho_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NACHO_H */

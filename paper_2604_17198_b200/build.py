@@ -1,0 +1,64 @@
+"""Builds the native pieces in-tree (no JIT cache): libnacho.so (sm_100a), the workload generator
+and the CPU oracle (test infrastructure).  Run by __graft_entry__.build()."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _newer(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _sources(d, exts=(".cu", ".cuh", ".h")):
+    out = []
+    for base, _, files in os.walk(d):
+        out += [os.path.join(base, f) for f in files if f.endswith(exts)]
+    return out
+
+
+def build_nacho(force=False, verbose=False):
+    out = os.path.join(HERE, "libnacho.so")
+    srcs = _sources(os.path.join(HERE, "csrc")) + [os.path.join(ROOT, "include", "nacho.h")]
+    if force or _newer(out, srcs):
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
+               "-I", os.path.join(ROOT, "include"), "-o", out, os.path.join(HERE, "csrc", "api.cu")]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.check_call(cmd)
+    return out
+
+
+def build_gen(force=False):
+    d = os.path.join(ROOT, "workloads")
+    out = os.path.join(d, "libnacho_gen.so")
+    src = os.path.join(d, "gen.cu")
+    if force or _newer(out, [src]):
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-o", out, src])
+    return out
+
+
+def build_oracle(force=False):
+    d = os.path.join(ROOT, "oracle")
+    out = os.path.join(d, "liboracle.so")
+    srcs = [os.path.join(d, "oracle.c"), os.path.join(d, "oracle.h")]
+    if force or _newer(out, srcs):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC", "-o", out, srcs[0]])
+    return out
+
+
+def build_all(force=False):
+    return [build_nacho(force), build_gen(force), build_oracle(force)]
+
+
+if __name__ == "__main__":
+    import sys
+    print(build_all(force="--force" in sys.argv))

@@ -1,0 +1,404 @@
+// api.cu -- the C ABI of libnacho.so (include/nacho.h): host-side validation, workspace carving
+// and kernel launches.  Every numeric step runs in the kernels of the included headers.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "partition.cuh"
+#include "spadd.cuh"
+#include "spmm.cuh"
+#include "spmv.cuh"
+
+using namespace nacho;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+nacho_status fail(nacho_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+nacho_status launched(const char* what) {
+  ++g_launches;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(NACHO_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return NACHO_SUCCESS;
+}
+
+#define NACHO_TRY(x)                          \
+  do {                                        \
+    const nacho_status _s = (x);              \
+    if (_s != NACHO_SUCCESS) return _s;       \
+  } while (0)
+
+constexpr int kSpmvThreads = 256;
+constexpr int kSpmvIptF32 = 16;   // 4096 positions per CTA
+constexpr int kSpmvIptF64 = 8;    // 2048
+constexpr int kSpaddThreads = 256;
+constexpr int kSpaddTile = 2048;  // entries (summed over operands) per CTA chunk
+constexpr int kSpmmWarps = 8;
+constexpr int kSpmmWitems = 128;  // 1024 positions per CTA
+constexpr int kPartWarps = 4;
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+int64_t spmv_tile(int dtype) { return dtype == NACHO_F64 ? kSpmvThreads * kSpmvIptF64 : kSpmvThreads * kSpmvIptF32; }
+
+nacho_status check_matrix(const nacho_matrix* A, const char* name) {
+  if (!A) return fail(NACHO_ERR_INVALID_ARG, "%s: null descriptor", name);
+  if (A->format != NACHO_CSR && A->format != NACHO_DCSR) return fail(NACHO_ERR_INVALID_ARG, "%s: bad format %d", name, A->format);
+  if (A->dtype != NACHO_F32 && A->dtype != NACHO_F64) return fail(NACHO_ERR_INVALID_ARG, "%s: bad dtype %d", name, A->dtype);
+  if (A->nrows < 0 || A->ncols < 0 || A->nnz < 0 || A->nouter < 0) return fail(NACHO_ERR_SHAPE, "%s: negative size", name);
+  if (A->ncols > INT32_MAX) return fail(NACHO_ERR_OVERFLOW, "%s: ncols %lld > INT32_MAX", name, (long long)A->ncols);
+  if (A->nrows >= (int64_t(1) << 32)) return fail(NACHO_ERR_OVERFLOW, "%s: nrows >= 2^32", name);
+  if (A->format == NACHO_CSR && A->nouter != A->nrows) return fail(NACHO_ERR_SHAPE, "%s: CSR needs nouter == nrows", name);
+  if (A->format == NACHO_DCSR && A->nouter > A->nrows) return fail(NACHO_ERR_SHAPE, "%s: DCSR nouter > nrows", name);
+  if (!A->pos) return fail(NACHO_ERR_INVALID_ARG, "%s: null pos", name);
+  if (A->nnz > 0 && (!A->crd || !A->val)) return fail(NACHO_ERR_INVALID_ARG, "%s: null crd/val", name);
+  if (A->format == NACHO_DCSR && A->nouter > 0 && !A->outer_crd) return fail(NACHO_ERR_INVALID_ARG, "%s: null outer_crd", name);
+  return NACHO_SUCCESS;
+}
+
+nacho_status check_ops(const nacho_matrix* ops, int32_t k) {
+  if (!ops) return fail(NACHO_ERR_INVALID_ARG, "null operand array");
+  if (k < 1 || k > NACHO_MAX_K) return fail(NACHO_ERR_INVALID_ARG, "k = %d outside [1, %d]", k, NACHO_MAX_K);
+  for (int o = 0; o < k; ++o) {
+    NACHO_TRY(check_matrix(ops + o, "operand"));
+    if (ops[o].format != ops[0].format || ops[o].nrows != ops[0].nrows || ops[o].ncols != ops[0].ncols ||
+        ops[o].dtype != ops[0].dtype)
+      return fail(NACHO_ERR_SHAPE, "operand %d disagrees with operand 0 in format/shape/dtype", o);
+  }
+  if (ops[0].format == NACHO_DCSR && k > 1) return fail(NACHO_ERR_INVALID_ARG, "DCSR partitioning supports k == 1");
+  return NACHO_SUCCESS;
+}
+
+OpsArg make_ops(const nacho_matrix* ops, int32_t k) {
+  OpsArg a;
+  memset(&a, 0, sizeof(a));
+  a.k = k;
+  a.dtype = ops[0].dtype;
+  a.nrows = ops[0].nrows;
+  a.ncols = ops[0].ncols;
+  for (int o = 0; o < k; ++o) {
+    a.op[o].pos = ops[o].pos;
+    a.op[o].crd = ops[o].crd;
+    a.op[o].val = ops[o].val;
+    a.op[o].outer = ops[o].format == NACHO_DCSR ? ops[o].outer_crd : nullptr;
+    a.op[o].nouter = ops[o].nouter;
+    a.op[o].nnz = ops[o].nnz;
+  }
+  return a;
+}
+
+int64_t total_cost(const nacho_matrix* ops, int32_t k) {  // a1: Q* = sum_o nnz_o
+  int64_t q = 0;
+  for (int o = 0; o < k; ++o) q += ops[o].nnz;
+  return q;
+}
+
+size_t parts_bytes(int64_t P, int k) {
+  return align_up((P + 1) * 8) * 3 + align_up((P + 1) * 4) + align_up((P + 1) * 8 * k);
+}
+
+PartsArg carve_parts(void* ws, int64_t P, int k) {
+  char* c = static_cast<char*>(ws);
+  PartsArg pa;
+  pa.P = (int32_t)P;
+  pa.k = k;
+  pa.query = reinterpret_cast<int64_t*>(c); c += align_up((P + 1) * 8);
+  pa.row = reinterpret_cast<int64_t*>(c); c += align_up((P + 1) * 8);
+  pa.row_pos = reinterpret_cast<int64_t*>(c); c += align_up((P + 1) * 8);
+  pa.col = reinterpret_cast<int32_t*>(c); c += align_up((P + 1) * 4);
+  pa.pos = reinterpret_cast<int64_t*>(c);
+  return pa;
+}
+
+PartsArg parts_arg(const nacho_parts* p) {
+  PartsArg pa;
+  pa.P = p->P; pa.k = p->k; pa.query = p->query; pa.row = p->row; pa.row_pos = p->row_pos;
+  pa.col = p->col; pa.pos = p->pos;
+  return pa;
+}
+
+nacho_status check_parts(const nacho_parts* p, int32_t k) {
+  if (!p) return fail(NACHO_ERR_INVALID_ARG, "null parts");
+  if (p->P < 1) return fail(NACHO_ERR_INVALID_ARG, "parts.P = %d < 1", p->P);
+  if (p->k != k) return fail(NACHO_ERR_INVALID_ARG, "parts.k = %d, expected %d", p->k, k);
+  if (!p->query || !p->row || !p->row_pos || !p->col || !p->pos) return fail(NACHO_ERR_INVALID_ARG, "parts: null array");
+  return NACHO_SUCCESS;
+}
+
+nacho_status launch_partition(const nacho_matrix* ops, int32_t k, const PartsArg& pa, cudaStream_t st) {
+  const OpsArg a = make_ops(ops, k);
+  const int64_t nb = (int64_t(pa.P) + 1 + kPartWarps - 1) / kPartWarps;
+  partition_kernel<kPartWarps><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, total_cost(ops, k));
+  return launched("partition_kernel");
+}
+
+int32_t auto_p(int64_t work, int64_t tile) {
+  int64_t P = (work + tile - 1) / tile;
+  if (P < 1) P = 1;
+  if (P > INT32_MAX - 1) P = INT32_MAX - 1;
+  return (int32_t)P;
+}
+
+template <typename T>
+nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, void* y, int32_t dense_y,
+                      char* ws_carry, cudaStream_t st) {
+  SpmvArgs<T> a;
+  a.pos = A->pos; a.crd = A->crd; a.val = static_cast<const T*>(A->val);
+  a.outer = A->format == NACHO_DCSR ? A->outer_crd : nullptr;
+  a.nouter = A->nouter;
+  a.x = static_cast<const T*>(x); a.y = static_cast<T*>(y);
+  a.dense_y = (A->format == NACHO_DCSR && dense_y) ? 1 : 0;
+  a.P = pa.P; a.ppos = pa.pos; a.prow = pa.row_pos;
+  a.carry_row = reinterpret_cast<int64_t*>(ws_carry);
+  a.carry_val = reinterpret_cast<T*>(ws_carry + align_up(int64_t(pa.P) * 8));
+  if (a.dense_y) {
+    if (cudaMemsetAsync(y, 0, sizeof(T) * A->nrows, st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "memset y");
+  }
+  if constexpr (sizeof(T) == 8) spmv_kernel<T, kSpmvThreads, kSpmvIptF64><<<pa.P, kSpmvThreads, 0, st>>>(a);
+  else spmv_kernel<T, kSpmvThreads, kSpmvIptF32><<<pa.P, kSpmvThreads, 0, st>>>(a);
+  NACHO_TRY(launched("spmv_kernel"));
+  const int64_t warps = (pa.P + 31) / 32;
+  spmv_fixup_kernel<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
+  return launched("spmv_fixup_kernel");
+}
+
+template <typename T, bool FILL>
+nacho_status launch_spadd(const SpaddArgs<T>& a, cudaStream_t st) {
+  auto kern = spadd_kernel<T, FILL, kSpaddThreads, kSpaddTile>;
+  const size_t smem = ((sizeof(SpaddShared<kSpaddThreads>) + 15) & ~size_t(15)) + 3 * kSpaddTile * 8 +
+                      (FILL ? 3 * kSpaddTile * sizeof(T) : 0);
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(spadd_kernel)");
+    configured = true;
+  }
+  kern<<<a.parts.P, kSpaddThreads, smem, st>>>(a);
+  return launched(FILL ? "spadd_fill_kernel" : "spadd_count_kernel");
+}
+
+template <typename T, int CPL, bool VEC>
+nacho_status launch_spmm(const SpmmArgs<T>& a, cudaStream_t st) {
+  spmm_kernel<T, CPL, VEC, kSpmmWarps, kSpmmWitems><<<a.P, kSpmmWarps * 32, 0, st>>>(a);
+  NACHO_TRY(launched("spmm_kernel"));
+  const int64_t warps = (a.P + 31) / 32;
+  spmm_fixup_kernel<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
+  return launched("spmm_fixup_kernel");
+}
+
+template <typename T>
+nacho_status run_spmm(const SpmmArgs<T>& a, cudaStream_t st) {
+  const int cpl = a.nb <= 32 ? 1 : a.nb <= 64 ? 2 : a.nb <= 128 ? 4 : 8;
+  const bool vec = (reinterpret_cast<uintptr_t>(a.B) % (cpl * sizeof(T)) == 0) && (a.ldb % cpl == 0);
+  switch (cpl) {
+    case 1: return launch_spmm<T, 1, false>(a, st);
+    case 2: return vec ? launch_spmm<T, 2, true>(a, st) : launch_spmm<T, 2, false>(a, st);
+    case 4:
+      if (sizeof(T) == 4) return vec ? launch_spmm<T, 4, true>(a, st) : launch_spmm<T, 4, false>(a, st);
+      return launch_spmm<T, 4, false>(a, st);
+    default: return launch_spmm<T, 8, false>(a, st);
+  }
+}
+
+__global__ void validate_kernel(nacho_matrix A, int* flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > A.nouter) return;
+  int bad = 0;
+  if (i == 0 && A.pos[0] != 0) bad = 1;
+  if (i == A.nouter && A.pos[A.nouter] != A.nnz) bad = 2;
+  if (i < A.nouter) {
+    const int64_t s = A.pos[i], e = A.pos[i + 1];
+    if (e < s || s < 0 || e > A.nnz) bad = 3;
+    else {
+      for (int64_t q = s; q < e && !bad; ++q) {
+        const int32_t c = A.crd[q];
+        if (c < 0 || c >= A.ncols) bad = 4;
+        if (q > s && c <= A.crd[q - 1]) bad = 5;
+      }
+    }
+    if (A.format == NACHO_DCSR) {
+      const int32_t r = A.outer_crd[i];
+      if (r < 0 || r >= A.nrows) bad = 6;
+      if (i > 0 && r <= A.outer_crd[i - 1]) bad = 7;
+      if (e == s) bad = 8;
+    }
+  }
+  if (bad) atomicMax(flag, bad);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nacho_last_error(void) { return g_err.c_str(); }
+
+int64_t nacho_launch_count(int32_t reset) {
+  const int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+nacho_status nacho_partition(const nacho_matrix* ops, int32_t k, int32_t P, nacho_parts* out, void* stream) {
+  NACHO_TRY(check_ops(ops, k));
+  if (P < 1) return fail(NACHO_ERR_INVALID_ARG, "P = %d < 1", P);
+  NACHO_TRY(check_parts(out, k));
+  if (out->P != P) return fail(NACHO_ERR_INVALID_ARG, "parts.P = %d != P = %d", out->P, P);
+  return launch_partition(ops, k, parts_arg(out), static_cast<cudaStream_t>(stream));
+}
+
+int32_t nacho_auto_partitions(const nacho_matrix* ops, int32_t k, int32_t op) {
+  if (!ops || k < 1) return 1;
+  const int64_t work = total_cost(ops, k);
+  if (op == 0) return auto_p(work, spmv_tile(ops[0].dtype));
+  if (op == 1) return auto_p(work, kSpaddTile - (k - 1));
+  return auto_p(work, kSpmmWarps * kSpmmWitems);
+}
+
+size_t nacho_spmv_workspace_size(const nacho_matrix* A, int32_t P) {
+  if (!A) return 0;
+  const bool auto_parts = P <= 0;
+  const int64_t Pe = auto_parts ? nacho_auto_partitions(A, 1, 0) : P;
+  const size_t vs = A->dtype == NACHO_F64 ? 8 : 4;
+  return align_up(Pe * 8) + align_up(Pe * vs) + (auto_parts ? parts_bytes(Pe, 1) : 0);
+}
+
+nacho_status nacho_spmv(const nacho_matrix* A, const nacho_parts* parts, const void* x, void* y, int32_t dense_y,
+                        void* ws, size_t ws_bytes, void* stream) {
+  NACHO_TRY(check_matrix(A, "A"));
+  if (!x && A->ncols > 0) return fail(NACHO_ERR_INVALID_ARG, "null x");
+  if (!y && (A->nouter > 0 || (dense_y && A->nrows > 0))) return fail(NACHO_ERR_INVALID_ARG, "null y");
+  if (parts) NACHO_TRY(check_parts(parts, 1));
+  const size_t need = nacho_spmv_workspace_size(A, parts ? parts->P : 0);
+  if (ws_bytes < need || (need > 0 && !ws)) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* c = static_cast<char*>(ws);
+  PartsArg pa;
+  if (parts) {
+    pa = parts_arg(parts);
+  } else {
+    const int64_t P = nacho_auto_partitions(A, 1, 0);
+    const size_t vs = A->dtype == NACHO_F64 ? 8 : 4;
+    pa = carve_parts(c + align_up(P * 8) + align_up(P * vs), P, 1);
+    NACHO_TRY(launch_partition(A, 1, pa, st));
+  }
+  if (A->dtype == NACHO_F64) return run_spmv<double>(A, pa, x, y, dense_y, c, st);
+  return run_spmv<float>(A, pa, x, y, dense_y, c, st);
+}
+
+size_t nacho_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {
+  (void)ops; (void)k;
+  return align_up((size_t)(P > 0 ? P : 1) * 8);
+}
+
+nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  NACHO_TRY(check_ops(ops, k));
+  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands");
+  NACHO_TRY(check_parts(parts, k));
+  if (!part_off) return fail(NACHO_ERR_INVALID_ARG, "null part_off");
+  const size_t need = nacho_spadd_k_workspace_size(ops, k, parts->P);
+  if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t* cnt = static_cast<int64_t*>(ws);
+  if (ops[0].dtype == NACHO_F64) {
+    SpaddArgs<double> a{make_ops(ops, k), parts_arg(parts), total_cost(ops, k), cnt, nullptr, nullptr, nullptr, nullptr};
+    NACHO_TRY((launch_spadd<double, false>(a, st)));
+  } else {
+    SpaddArgs<float> a{make_ops(ops, k), parts_arg(parts), total_cost(ops, k), cnt, nullptr, nullptr, nullptr, nullptr};
+    NACHO_TRY((launch_spadd<float, false>(a, st)));
+  }
+  scan_counts_kernel<1024><<<1, 1024, 0, st>>>(cnt, parts->P, part_off);
+  return launched("scan_counts_kernel");
+}
+
+nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_parts* parts,
+                                const int64_t* part_off, int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws,
+                                size_t ws_bytes, void* stream) {
+  (void)ws; (void)ws_bytes;
+  NACHO_TRY(check_ops(ops, k));
+  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands");
+  NACHO_TRY(check_parts(parts, k));
+  if (!part_off || !z_pos) return fail(NACHO_ERR_INVALID_ARG, "null part_off / z_pos");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (ops[0].dtype == NACHO_F64) {
+    SpaddArgs<double> a{make_ops(ops, k), parts_arg(parts), total_cost(ops, k), nullptr, part_off, z_pos, z_crd,
+                        static_cast<double*>(z_val)};
+    return launch_spadd<double, true>(a, st);
+  }
+  SpaddArgs<float> a{make_ops(ops, k), parts_arg(parts), total_cost(ops, k), nullptr, part_off, z_pos, z_crd,
+                     static_cast<float*>(z_val)};
+  return launch_spadd<float, true>(a, st);
+}
+
+size_t nacho_spmm_workspace_size(const nacho_matrix* A, int32_t P, int32_t nb) {
+  if (!A) return 0;
+  const bool auto_parts = P <= 0;
+  const int64_t Pe = auto_parts ? nacho_auto_partitions(A, 1, 2) : P;
+  const size_t vs = A->dtype == NACHO_F64 ? 8 : 4;
+  return align_up(Pe * 8) + align_up(Pe * vs * (nb > 0 ? nb : 1)) + (auto_parts ? parts_bytes(Pe, 1) : 0);
+}
+
+nacho_status nacho_spmm(const nacho_matrix* A, const nacho_parts* parts, const void* B, int64_t ldb, int32_t nb,
+                        void* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
+  NACHO_TRY(check_matrix(A, "A"));
+  if (A->format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "SpMM supports CSR");
+  if (nb < 1 || nb > 256) return fail(NACHO_ERR_INVALID_ARG, "nb = %d outside [1, 256]", nb);
+  if (ldb < nb || ldc < nb) return fail(NACHO_ERR_SHAPE, "ldb/ldc < nb");
+  if ((!B && A->ncols > 0) || (!C && A->nrows > 0)) return fail(NACHO_ERR_INVALID_ARG, "null B/C");
+  if (parts) NACHO_TRY(check_parts(parts, 1));
+  const size_t need = nacho_spmm_workspace_size(A, parts ? parts->P : 0, nb);
+  if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* c = static_cast<char*>(ws);
+  const int64_t P = parts ? parts->P : nacho_auto_partitions(A, 1, 2);
+  const size_t vs = A->dtype == NACHO_F64 ? 8 : 4;
+  PartsArg pa;
+  if (parts) pa = parts_arg(parts);
+  else {
+    pa = carve_parts(c + align_up(P * 8) + align_up(P * vs * nb), P, 1);
+    NACHO_TRY(launch_partition(A, 1, pa, st));
+  }
+  if (A->dtype == NACHO_F64) {
+    SpmmArgs<double> a{A->pos, A->crd, static_cast<const double*>(A->val), A->nrows, static_cast<const double*>(B), ldb,
+                       nb, static_cast<double*>(C), ldc, pa.P, pa.pos, pa.row_pos,
+                       reinterpret_cast<int64_t*>(c), reinterpret_cast<double*>(c + align_up(P * 8))};
+    return run_spmm<double>(a, st);
+  }
+  SpmmArgs<float> a{A->pos, A->crd, static_cast<const float*>(A->val), A->nrows, static_cast<const float*>(B), ldb,
+                    nb, static_cast<float*>(C), ldc, pa.P, pa.pos, pa.row_pos,
+                    reinterpret_cast<int64_t*>(c), reinterpret_cast<float*>(c + align_up(P * 8))};
+  return run_spmm<float>(a, st);
+}
+
+nacho_status nacho_validate(const nacho_matrix* A, void* stream) {
+  NACHO_TRY(check_matrix(A, "A"));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* flag = nullptr;
+  if (cudaMallocAsync(&flag, sizeof(int), st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "cudaMallocAsync");
+  cudaMemsetAsync(flag, 0, sizeof(int), st);
+  const int64_t n = A->nouter + 1;
+  validate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(*A, flag);
+  nacho_status s = launched("validate_kernel");
+  int h = 0;
+  cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(flag, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "validate sync");
+  if (s != NACHO_SUCCESS) return s;
+  if (h) return fail(NACHO_ERR_FORMAT, "format invariant %d violated", h);
+  return NACHO_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+// common.cuh -- device-side types and warp/block primitives shared by the libnacho kernels.
+// (Nothing here is shared with the oracle.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/nacho.h"
+
+namespace nacho {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// One sparse operand as the kernels see it: pos in the outer-position space
+// [0, nouter], crd/val in position space.  outer != nullptr <=> DCSR.
+struct OpView {
+  const int64_t* pos;
+  const int32_t* crd;
+  const void* val;
+  const int32_t* outer;
+  int64_t nouter;
+  int64_t nnz;
+};
+
+// Up to NACHO_MAX_K operands passed by value to kernels.
+struct OpsArg {
+  OpView op[NACHO_MAX_K];
+  int32_t k;
+  int32_t dtype;
+  int64_t nrows, ncols;
+};
+
+// Partition record (device pointers), see nacho_parts.
+struct PartsArg {
+  int32_t P, k;
+  int64_t* query;
+  int64_t* row;
+  int64_t* row_pos;
+  int32_t* col;
+  int64_t* pos;
+};
+
+// Q_p = floor(p * Q* / P) without 128-bit arithmetic: (Q*/P)*p + ((Q*%P)*p)/P is exact because
+// (Q*%P)*p < P*P <= 2^62 (reading R4).
+__host__ __device__ __forceinline__ int64_t query_of(int64_t qstar, int64_t P, int64_t p) {
+  return (qstar / P) * p + ((qstar % P) * p) / P;
+}
+
+template <typename T>
+__device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+
+// ------------------------------------------------------------------ warp 32-ary search
+// Largest x in [lo, hi] with pred(x) true, given pred(lo) true and pred monotone (true...false).
+// Each round probes 32 evenly spaced candidates (one per lane) and keeps the bracket between the
+// last accepted and the first rejected probe: ceil(log32(hi-lo+1)) rounds of one probe per lane.
+template <typename Pred>
+__device__ __forceinline__ int64_t warp_highest_true(int64_t lo, int64_t hi, Pred pred) {
+  const int lane = threadIdx.x & 31;
+  while (hi > lo) {
+    const int64_t span = hi - lo;
+    int64_t x = (span <= 32) ? lo + lane + 1 : lo + (((int64_t)(lane + 1) * span + 31) >> 5);
+    if (x > hi) x = hi;
+    const bool ok = pred(x);
+    const unsigned m = __ballot_sync(kFull, ok);
+    const int64_t x0 = __shfl_sync(kFull, x, 0);
+    if (m == 0) { hi = x0 - 1; continue; }
+    const int j = 31 - __clz(m);
+    const int64_t xj = __shfl_sync(kFull, x, j);
+    const int64_t xn = __shfl_sync(kFull, x, j < 31 ? j + 1 : 31);
+    lo = xj;
+    if (j < 31 && xn > xj) hi = xn - 1;
+  }
+  return lo;
+}
+
+// lower bound: least p in [lo, hi+1] with crd[p] >= v (lb_search of Listing 7).
+__device__ __forceinline__ int64_t lb_search(const int32_t* __restrict__ crd, int64_t lo, int64_t hi, int64_t v) {
+  int64_t a = lo, b = hi + 1;
+  while (a < b) {
+    const int64_t m = a + ((b - a) >> 1);
+    if ((int64_t)ldg(crd + m) >= v) b = m; else a = m + 1;
+  }
+  return a;
+}
+
+// ------------------------------------------------------------------ boundary search
+struct Boundary {
+  int64_t row;       // row coordinate
+  int64_t row_pos;   // outer position
+  int32_t col;
+  int64_t pos[NACHO_MAX_K];
+};
+
+__device__ __forceinline__ void set_end(const OpsArg& a, Boundary& b) {
+  b.row = a.nrows;
+  b.row_pos = a.op[0].nouter;
+  b.col = 0;
+#pragma unroll
+  for (int o = 0; o < NACHO_MAX_K; ++o) if (o < a.k) b.pos[o] = a.op[o].nnz;
+}
+
+__device__ __forceinline__ void set_origin(const OpsArg& a, Boundary& b) {
+  b.row = 0; b.row_pos = 0; b.col = 0;
+#pragma unroll
+  for (int o = 0; o < NACHO_MAX_K; ++o) if (o < a.k) b.pos[o] = 0;
+}
+
+// FindPartition (Alg. 1) for query Q, executed by one full warp; every lane returns
+// the same boundary.  Level i (rows): highest outer position x with sum_o pos_o[x] <= Q (Listing 5
+// C_i; for DCSR the compressed row level is searched in its position space).  Level j:
+// residual R = Q - C_i(x); one operand -> the position is Q itself (position space);
+// k operands -> the highest column v with sum_o (lb_o(v) - seg_o) <= R, found by a 32-ary search
+// over column values in which every lane runs the per-operand lb_search of Listing 7 inside windows
+// that narrow round by round.
+__device__ __noinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t Q, int64_t outer_lo, int64_t outer_hi) {
+  Boundary b;
+  const int k = a.k;
+  // ---- level i
+  auto outer_ok = [&](int64_t x) {
+    int64_t s = 0;
+#pragma unroll
+    for (int o = 0; o < NACHO_MAX_K; ++o) if (o < k) s += ldg(a.op[o].pos + x);
+    return s <= Q;
+  };
+  const int64_t x = warp_highest_true(outer_lo, outer_hi, outer_ok);
+  if (x >= a.op[0].nouter) { set_end(a, b); return b; }
+  b.row_pos = x;
+  b.row = a.op[0].outer ? (int64_t)ldg(a.op[0].outer + x) : x;
+  if (k == 1) {
+    b.pos[0] = Q;
+    b.col = ldg(a.op[0].crd + Q);
+    return b;
+  }
+  // ---- level j (k-way order statistic of the row's column segments)
+  int64_t seg[NACHO_MAX_K], wlo[NACHO_MAX_K], whi[NACHO_MAX_K];
+  int64_t R = Q;
+  int64_t vlo = INT64_MAX, vhi = -1;
+#pragma unroll
+  for (int o = 0; o < NACHO_MAX_K; ++o) {
+    if (o < k) {
+      seg[o] = ldg(a.op[o].pos + x);
+      const int64_t e = ldg(a.op[o].pos + x + 1);
+      R -= seg[o];
+      wlo[o] = seg[o];
+      whi[o] = e - 1;
+      if (e > seg[o]) {
+        const int64_t f = ldg(a.op[o].crd + seg[o]), l = ldg(a.op[o].crd + e - 1);
+        vlo = f < vlo ? f : vlo;
+        vhi = l > vhi ? l : vhi;
+      }
+    }
+  }
+  // cnt(vlo) = 0 <= R: vlo (the smallest stored column) is an admissible start of the bracket.
+  const int lane = threadIdx.x & 31;
+  while (vhi > vlo) {
+    const int64_t span = vhi - vlo;
+    int64_t v = (span <= 32) ? vlo + lane + 1 : vlo + (((int64_t)(lane + 1) * span + 31) >> 5);
+    if (v > vhi) v = vhi;
+    int64_t lb[NACHO_MAX_K];
+    int64_t cnt = 0;
+#pragma unroll
+    for (int o = 0; o < NACHO_MAX_K; ++o) {
+      if (o < k) {
+        lb[o] = lb_search(a.op[o].crd, wlo[o], whi[o], v);
+        cnt += lb[o] - seg[o];
+      }
+    }
+    const unsigned m = __ballot_sync(kFull, cnt <= R);
+    if (m == 0) {
+      const int64_t v0 = __shfl_sync(kFull, v, 0);
+#pragma unroll
+      for (int o = 0; o < NACHO_MAX_K; ++o) if (o < k) whi[o] = __shfl_sync(kFull, lb[o], 0) - 1;
+      vhi = v0 - 1;
+      continue;
+    }
+    const int j = 31 - __clz(m);
+    const int jn = j < 31 ? j + 1 : 31;
+    const int64_t vj = __shfl_sync(kFull, v, j), vn = __shfl_sync(kFull, v, jn);
+#pragma unroll
+    for (int o = 0; o < NACHO_MAX_K; ++o) {
+      if (o < k) {
+        const int64_t lj = __shfl_sync(kFull, lb[o], j), ln = __shfl_sync(kFull, lb[o], jn);
+        wlo[o] = lj;
+        if (j < 31 && vn > vj) whi[o] = ln - 1;
+      }
+    }
+    vlo = vj;
+    if (j < 31 && vn > vj) vhi = vn - 1;
+  }
+  b.col = (int32_t)vlo;
+#pragma unroll
+  for (int o = 0; o < NACHO_MAX_K; ++o) if (o < k) b.pos[o] = wlo[o];
+  return b;
+}
+
+// ------------------------------------------------------------------ scans
+template <typename T>
+__device__ __forceinline__ T warp_incl_sum(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const T u = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v += u;
+  }
+  return v;
+}
+
+// Block-wide exclusive sum of one value per thread; returns the exclusive prefix and writes the
+// block total to *total.  `red` must hold >= THREADS/32 elements of shared memory.
+template <int THREADS, typename T>
+__device__ __forceinline__ T block_excl_sum(T v, T* red, T* total) {
+  constexpr int W = THREADS / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const T inc = warp_incl_sum(v);
+  if (lane == 31) red[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T t = lane < W ? red[lane] : T(0);
+    const T ti = warp_incl_sum(t);
+    if (lane < W) red[lane] = ti - t;  // exclusive warp offsets
+    if (lane == W - 1) red[W] = ti;
+  }
+  __syncthreads();
+  const T res = red[w] + inc - v;
+  *total = red[W];
+  __syncthreads();
+  return res;
+}
+
+}  // namespace nacho
