@@ -27,6 +27,8 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+METRIC = "GNNZ/s (3-way CSR SpAdd A+B+C on C2: partition + assembly + compute), % of HBM roofline"
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -167,6 +169,16 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
         N.partition(ops, P, out=parts)
         if timed:
             m.append(ev(torch))
+        N.spadd_k_fused(ops, local, z_pos, z_crd, z_val, part_off=part_off, ws=ws)
+        if timed:
+            m.append(ev(torch))
+        return m
+
+    def step2(timed=False):  # the paper's two-pass assembly (count -> scan -> fill), for comparison
+        m = [ev(torch)] if timed else None
+        N.partition(ops, P, out=parts)
+        if timed:
+            m.append(ev(torch))
         N.spadd_k_count(ops, local, part_off, ws)
         if timed:
             m.append(ev(torch))
@@ -175,7 +187,8 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
             m.append(ev(torch))
         return m
 
-    sections = ["partition", "count+scan", "fill"]
+    sections = ["partition", "spadd_fused"]
+    t2, sec2 = timer.run(step2, 5, 2, ["partition", "count+scan", "fill"])
     step()
     torch.cuda.synchronize()
     N.launch_count(reset=True)
@@ -185,12 +198,12 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
     nnz_z = int(part_off[-1].item())
     vs = ops[0].val.element_size()
     algo_step = sum(n * (4 + vs) + (M + 1) * 8 for n in nnz) + nnz_z * (4 + vs) + (M + 1) * 8
-    fill_bytes = sum(n * (4 + vs) + (M + 1) * 8 for n in nnz) + nnz_z * (4 + vs) + (M + 1) * 8
-    count_bytes = sum(n * 4 + (M + 1) * 8 for n in nnz)
+    fused_bytes = sum(n * (4 + vs) + (M + 1) * 8 for n in nnz) + nnz_z * (4 + vs) + (M + 1) * 8
     res = dict(work=qstar / world if world > 1 else qstar, times=times, sec=sec, launches=launches,
                algo_step=algo_step, nnz_z=nnz_z, P=P,
-               kernel_bytes={"fill": fill_bytes, "count+scan": count_bytes,
-                             "partition": (P + 1) * (8 * k + 28)},
+               kernel_bytes={"spadd_fused": fused_bytes, "partition": (P + 1) * (8 * k + 28)},
+               two_pass={"ms_per_step": statistics.mean(t2),
+                         "sections_ms": {s: statistics.mean(v) for s, v in sec2.items()}},
                dtype="f32" if vs == 4 else "f64", wl=wl, parts=parts)
     return res
 
@@ -213,10 +226,11 @@ def e2e_spadd(N, torch, wl, args):
             for a, b in zip(h, d):
                 b.copy_(a, non_blocking=True)
         N.partition(ops, P, out=parts)
-        z_pos, z_crd, z_val = N.spadd_k(ops, parts)          # host reads nnz_Z (two-pass)
+        z_pos, z_crd, z_val = N.spadd_k_fused(ops, parts)
         out_host["pos"] = z_pos.cpu()
-        out_host["crd"] = z_crd.cpu()
-        out_host["val"] = z_val.cpu()
+        nz = int(out_host["pos"][-1])
+        out_host["crd"] = z_crd[:nz].cpu()
+        out_host["val"] = z_val[:nz].cpu()
 
     for _ in range(max(1, args.warmup)):
         step()
@@ -343,7 +357,7 @@ def run_reference(args):
     ts = [oracle_spadd_once(O, host, P) for _ in range(args.steps)]
     ms = statistics.mean(ts) * 1e3
     v = qstar / (ms * 1e-3) / 1e9
-    line = {"impl": "reference", "metric": "GNNZ/s (3-way CSR SpAdd A+B+C, C2)", "value": v, "unit": "GNNZ/s",
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GNNZ/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "c2_spadd3_1Mx1M_3x1e7nnz", "scale": args.scale},
@@ -390,7 +404,7 @@ def main():
     summ, dom, dms, achieved = summarize(r, peak)
     tt = traffic_table().get(f"c2:{dom}")
     line = {
-        "metric": "GNNZ/s (3-way CSR SpAdd A+B+C: partition + count/scan + fill), % of HBM roofline",
+        "metric": METRIC,
         "value": sum(A.nnz for A in r["wl"].ops) / (ms * 1e-3) / 1e9,
         "unit": "GNNZ/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
@@ -403,6 +417,7 @@ def main():
                      "algorithmic_bytes_per_launch": r["kernel_bytes"][dom]},
         "step_roofline_frac": summ["step_hbm_frac"],
         "sections_ms": summ["sections_ms"],
+        "two_pass": r["two_pass"],
         "gpu_launches": r["launches"] * args.steps,
         "clocks": clk,
     }

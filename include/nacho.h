@@ -122,6 +122,17 @@ nacho_status nacho_spmv(const nacho_matrix* A, const nacho_parts* parts, const v
  *   part_off [P+1] int64 (device).   z_pos [nrows+1] int64.   z_crd [nnz_Z] int32, z_val [nnz_Z].
  *   ws       >= nacho_spadd_k_workspace_size(ops, k, P). */
 size_t nacho_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P);
+/* nacho_spadd_k -- the same Z in ONE pass: every partition merges its staged operand ranges once,
+ * obtains its write offset from a decoupled look-back over the partitions (single-pass prefix
+ * sum) and writes Z immediately, so assembly and compute share one read of the operands
+ * and no host round trip separates them.  z_crd / z_val must hold Q* = sum_o nnz_o entries (an
+ * upper bound of nnz_Z, reading "Allocation" of Fig. 7a as an upper-bound allocation); nnz_Z is
+ * z_pos[nrows] (and part_off[P] when part_off != NULL, which then receives every partition's
+ * offset).  Partitions must hold at most 2048 entries (nacho_auto_partitions(ops, k, 1) does);
+ * larger ones return NACHO_ERR_INVALID_ARG -- use the two-pass calls.
+ *   ws  >= nacho_spadd_k_workspace_size(ops, k, P) bytes (look-back flags). */
+nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
+                           int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes, void* stream);
 nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
                                  void* ws, size_t ws_bytes, void* stream);
 nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_parts* parts,

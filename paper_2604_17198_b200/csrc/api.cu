@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "partition.cuh"
 #include "spadd.cuh"
+#include "spadd3.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
 
@@ -190,6 +191,38 @@ nacho_status launch_spadd(const SpaddArgs<T>& a, cudaStream_t st) {
   return launched(FILL ? "spadd_fill_kernel" : "spadd_count_kernel");
 }
 
+// Persistent warp-specialised SpAdd (spadd2.cuh): grid = resident CTAs (look-back needs them all
+// co-resident), each CTA walks partitions blockIdx.x, +gridDim.x, ...
+template <typename T, int MODE>
+nacho_status launch_spadd2(const Spadd2Args<T>& a, cudaStream_t st) {
+  auto kern = spadd2_kernel<T, MODE>;
+  const size_t smem = sa_smem_bytes<T>(a.ops.k, MODE != kCount);
+  static int occ = -1;
+  static size_t occ_smem = 0;
+  if (occ < 0 || occ_smem != smem) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(spadd2_kernel)");
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kSaThreads, smem) != cudaSuccess || blocks < 1)
+      return fail(NACHO_ERR_CUDA, "spadd2_kernel does not fit an SM (%zu bytes of shared memory)", smem);
+    occ = blocks;
+    occ_smem = smem;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = (int64_t)sms * occ;
+  if (grid > a.parts.P) grid = a.parts.P;
+  kern<<<(unsigned)grid, kSaThreads, smem, st>>>(a);
+  return launched(MODE == kCount ? "spadd2_count" : MODE == kFill ? "spadd2_fill" : "spadd2_fused");
+}
+
+// Largest possible partition of a k-operand partition with P parts (Theorem 1 slack k-1).
+bool fits_sa_tile(const nacho_matrix* ops, int32_t k, int32_t P) {
+  const int64_t q = total_cost(ops, k);
+  return (q + P - 1) / P + (k - 1) <= kSaTile;
+}
+
 template <typename T, int CPL, bool VEC>
 nacho_status launch_spmm(const SpmmArgs<T>& a, cudaStream_t st) {
   spmm_kernel<T, CPL, VEC, kSpmmWarps, kSpmmWitems><<<a.P, kSpmmWarps * 32, 0, st>>>(a);
@@ -244,6 +277,18 @@ __global__ void validate_kernel(nacho_matrix A, int* flag) {
 extern "C" {
 
 const char* nacho_last_error(void) { return g_err.c_str(); }
+
+// Debug only (not part of nacho.h): the spadd2 phase timers of a -DNACHO_PROF build.
+int nacho_debug_phases(unsigned long long* out, int reset) {
+#ifdef NACHO_PROF
+  cudaMemcpyFromSymbol(out, g_phase, sizeof(g_phase));
+  if (reset) { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_phase, z, sizeof(z)); }
+  return 1;
+#else
+  (void)out; (void)reset;
+  return 0;
+#endif
+}
 
 int64_t nacho_launch_count(int32_t reset) {
   const int64_t v = g_launches;
@@ -300,7 +345,7 @@ nacho_status nacho_spmv(const nacho_matrix* A, const nacho_parts* parts, const v
 
 size_t nacho_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {
   (void)ops; (void)k;
-  return align_up((size_t)(P > 0 ? P : 1) * 8);
+  return align_up((size_t)((P > 0 ? P : 1) + 1) * 8);
 }
 
 nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
@@ -313,7 +358,15 @@ nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho
   if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t* cnt = static_cast<int64_t*>(ws);
-  if (ops[0].dtype == NACHO_F64) {
+  if (fits_sa_tile(ops, k, parts->P)) {
+    if (ops[0].dtype == NACHO_F64) {
+      Spadd2Args<double> a{make_ops(ops, k), parts_arg(parts), cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+      NACHO_TRY((launch_spadd2<double, kCount>(a, st)));
+    } else {
+      Spadd2Args<float> a{make_ops(ops, k), parts_arg(parts), cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+      NACHO_TRY((launch_spadd2<float, kCount>(a, st)));
+    }
+  } else if (ops[0].dtype == NACHO_F64) {
     SpaddArgs<double> a{make_ops(ops, k), parts_arg(parts), total_cost(ops, k), cnt, nullptr, nullptr, nullptr, nullptr};
     NACHO_TRY((launch_spadd<double, false>(a, st)));
   } else {
@@ -333,6 +386,16 @@ nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_
   NACHO_TRY(check_parts(parts, k));
   if (!part_off || !z_pos) return fail(NACHO_ERR_INVALID_ARG, "null part_off / z_pos");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (fits_sa_tile(ops, k, parts->P)) {
+    if (ops[0].dtype == NACHO_F64) {
+      Spadd2Args<double> a{make_ops(ops, k), parts_arg(parts), nullptr, const_cast<int64_t*>(part_off), nullptr, nullptr, z_pos,
+                           z_crd, static_cast<double*>(z_val)};
+      return launch_spadd2<double, kFill>(a, st);
+    }
+    Spadd2Args<float> a{make_ops(ops, k), parts_arg(parts), nullptr, const_cast<int64_t*>(part_off), nullptr, nullptr, z_pos,
+                        z_crd, static_cast<float*>(z_val)};
+    return launch_spadd2<float, kFill>(a, st);
+  }
   if (ops[0].dtype == NACHO_F64) {
     SpaddArgs<double> a{make_ops(ops, k), parts_arg(parts), total_cost(ops, k), nullptr, part_off, z_pos, z_crd,
                         static_cast<double*>(z_val)};
@@ -341,6 +404,31 @@ nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_
   SpaddArgs<float> a{make_ops(ops, k), parts_arg(parts), total_cost(ops, k), nullptr, part_off, z_pos, z_crd,
                      static_cast<float*>(z_val)};
   return launch_spadd<float, true>(a, st);
+}
+
+nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
+                           int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes, void* stream) {
+  NACHO_TRY(check_ops(ops, k));
+  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands");
+  NACHO_TRY(check_parts(parts, k));
+  if (!z_pos) return fail(NACHO_ERR_INVALID_ARG, "null z_pos");
+  if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
+  if (!fits_sa_tile(ops, k, parts->P))
+    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kSaTile);
+  const size_t need = nacho_spadd_k_workspace_size(ops, k, parts->P);
+  if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto* flags = static_cast<unsigned long long*>(ws);
+  if (cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * (parts->P + 1), st) != cudaSuccess)
+    return fail(NACHO_ERR_CUDA, "memset look-back flags");
+  if (ops[0].dtype == NACHO_F64) {
+    Spadd2Args<double> a{make_ops(ops, k), parts_arg(parts), nullptr, part_off, flags, flags + parts->P, z_pos, z_crd,
+                         static_cast<double*>(z_val)};
+    return launch_spadd2<double, kFused>(a, st);
+  }
+  Spadd2Args<float> a{make_ops(ops, k), parts_arg(parts), nullptr, part_off, flags, flags + parts->P, z_pos, z_crd,
+                      static_cast<float*>(z_val)};
+  return launch_spadd2<float, kFused>(a, st);
 }
 
 size_t nacho_spmm_workspace_size(const nacho_matrix* A, int32_t P, int32_t nb) {

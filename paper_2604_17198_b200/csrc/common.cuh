@@ -105,6 +105,115 @@ __device__ __forceinline__ void set_origin(const OpsArg& a, Boundary& b) {
   for (int o = 0; o < NACHO_MAX_K; ++o) if (o < a.k) b.pos[o] = 0;
 }
 
+// #lanes c in [0, n) (n <= 32) with v(c) < x, for a per-lane value v non-decreasing over lanes and a
+// per-lane query x (binary search over lanes with shuffles; all lanes execute every shuffle).
+__device__ __forceinline__ int lanes_less(int64_t v, int64_t x, int n) {
+  int lo = 0, hi = n;
+#pragma unroll
+  for (int it = 0; it < 6; ++it) {
+    const int mid = (lo + hi) >> 1;
+    const int64_t vm = __shfl_sync(kFull, v, mid & 31);
+    if (lo < hi) { if (vm < x) lo = mid + 1; else hi = mid; }
+  }
+  return lo;
+}
+
+// The (R+1)-th smallest column of the multiset union of the windows crd_o[lo_o, hi_o) (one row
+// segment per operand) and its lower-bound position in every operand -- the inner level of
+// FindPartition for k operands.  Invariant: entries left of lo_o are smaller than the answer v*,
+// entries at or after hi_o are larger, and v* is the R-th (0-based) of the windows' union.
+// Each round samples 32 positions of every window (one load per lane and operand, all in flight
+// at once); the samples of the largest window are candidate values whose rank is bracketed from
+// the other windows' samples; the bracket that provably contains v* becomes the new windows
+// (shrinking them ~33/(k+1)-fold).  Once every window holds <= 32 entries the answer is resolved
+// exactly with lane shuffles.
+__device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&lo)[NACHO_MAX_K],
+                                              int64_t (&hi)[NACHO_MAX_K], int64_t R, Boundary& b) {
+  const int lane = threadIdx.x & 31;
+  constexpr int64_t INF = INT64_MAX;
+  for (;;) {
+    int m = 0;
+    int64_t lmax = -1;
+#pragma unroll
+    for (int o = 0; o < NACHO_MAX_K; ++o)
+      if (o < k && hi[o] - lo[o] > lmax) { lmax = hi[o] - lo[o]; m = o; }
+    if (lmax <= 32) break;
+    int64_t sp[NACHO_MAX_K], u[NACHO_MAX_K];
+#pragma unroll
+    for (int o = 0; o < NACHO_MAX_K; ++o) {
+      if (o < k) {
+        const int64_t len = hi[o] - lo[o];
+        if (len > 0) { sp[o] = lo[o] + ((int64_t)(lane + 1) * len) / 33; u[o] = ldg(a.op[o].crd + sp[o]); }
+        else { sp[o] = lo[o]; u[o] = INF; }
+      }
+    }
+    int64_t cand = 0, own = 0, spm = 0;
+#pragma unroll
+    for (int o = 0; o < NACHO_MAX_K; ++o)
+      if (o == m) { cand = u[o]; spm = sp[o]; own = sp[o] - lo[o]; }
+    int64_t L = own, U = own;
+    int64_t Lo[NACHO_MAX_K], Uo[NACHO_MAX_K];
+#pragma unroll
+    for (int o = 0; o < NACHO_MAX_K; ++o) {
+      if (o < k) {
+        const int64_t len = hi[o] - lo[o];
+        const int j = lanes_less(u[o], cand, len > 0 ? 32 : 0);
+        const int64_t sjm = __shfl_sync(kFull, sp[o], j > 0 ? j - 1 : 0);
+        const int64_t sj = __shfl_sync(kFull, sp[o], j < 32 ? j : 31);
+        Lo[o] = j > 0 ? sjm - lo[o] + 1 : 0;
+        Uo[o] = j < 32 ? sj - lo[o] : len;
+        if (o != m) { L += Lo[o]; U += Uo[o]; }
+      }
+    }
+    const unsigned below = __ballot_sync(kFull, U <= R);   // candidates <= v*
+    const unsigned above = __ballot_sync(kFull, L > R);    // candidates >  v*
+    const int ia = below ? 31 - __clz(below) : -1;
+    const int ib = above ? __ffs(above) - 1 : 32;
+    int64_t drop = 0;
+#pragma unroll
+    for (int o = 0; o < NACHO_MAX_K; ++o) {
+      if (o < k) {
+        const int64_t la = __shfl_sync(kFull, o == m ? spm - lo[o] : Lo[o], ia >= 0 ? ia : 0);
+        const int64_t ub = __shfl_sync(kFull, o == m ? spm - lo[o] : Uo[o], ib < 32 ? ib : 0);
+        const int64_t nlo = ia >= 0 ? lo[o] + la : lo[o];
+        const int64_t nhi = ib < 32 ? lo[o] + ub : hi[o];
+        drop += nlo - lo[o];
+        lo[o] = nlo;
+        hi[o] = nhi;
+      }
+    }
+    R -= drop;
+  }
+  // ---- exact resolution: every window holds <= 32 entries, lane l holds entry l of each
+  int64_t e[NACHO_MAX_K];
+#pragma unroll
+  for (int o = 0; o < NACHO_MAX_K; ++o)
+    if (o < k) e[o] = (lane < hi[o] - lo[o]) ? (int64_t)ldg(a.op[o].crd + lo[o] + lane) : INF;
+  int64_t vstar = INF;
+  bool found = false;
+#pragma unroll
+  for (int o = 0; o < NACHO_MAX_K; ++o) {
+    if (o < k) {
+      int64_t less = 0, leq = 0;
+#pragma unroll
+      for (int o2 = 0; o2 < NACHO_MAX_K; ++o2) {
+        if (o2 < k) {
+          const int n2 = (int)(hi[o2] - lo[o2]);
+          less += lanes_less(e[o2], e[o], n2);
+          leq += lanes_less(e[o2], e[o] == INF ? INF : e[o] + 1, n2);
+        }
+      }
+      const bool hit = e[o] != INF && less <= R && R < leq;
+      const unsigned hm = __ballot_sync(kFull, hit);
+      if (hm && !found) { vstar = __shfl_sync(kFull, e[o], __ffs(hm) - 1); found = true; }
+    }
+  }
+  b.col = (int32_t)vstar;
+#pragma unroll
+  for (int o = 0; o < NACHO_MAX_K; ++o)
+    if (o < k) b.pos[o] = lo[o] + __popc(__ballot_sync(kFull, e[o] < vstar));
+}
+
 // FindPartition (Alg. 1) for query Q, executed by one full warp; every lane returns
 // the same boundary.  Level i (rows): highest outer position x with sum_o pos_o[x] <= Q (Listing 5
 // C_i; for DCSR the compressed row level is searched in its position space).  Level j:
@@ -131,65 +240,18 @@ __device__ __noinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t Q, 
     b.col = ldg(a.op[0].crd + Q);
     return b;
   }
-  // ---- level j (k-way order statistic of the row's column segments)
-  int64_t seg[NACHO_MAX_K], wlo[NACHO_MAX_K], whi[NACHO_MAX_K];
+  // ---- level j: the (R+1)-th smallest column of the multiset union of the row's k segments
+  int64_t lo[NACHO_MAX_K], hi[NACHO_MAX_K];
   int64_t R = Q;
-  int64_t vlo = INT64_MAX, vhi = -1;
 #pragma unroll
   for (int o = 0; o < NACHO_MAX_K; ++o) {
     if (o < k) {
-      seg[o] = ldg(a.op[o].pos + x);
-      const int64_t e = ldg(a.op[o].pos + x + 1);
-      R -= seg[o];
-      wlo[o] = seg[o];
-      whi[o] = e - 1;
-      if (e > seg[o]) {
-        const int64_t f = ldg(a.op[o].crd + seg[o]), l = ldg(a.op[o].crd + e - 1);
-        vlo = f < vlo ? f : vlo;
-        vhi = l > vhi ? l : vhi;
-      }
+      lo[o] = ldg(a.op[o].pos + x);
+      hi[o] = ldg(a.op[o].pos + x + 1);
+      R -= lo[o];
     }
   }
-  // cnt(vlo) = 0 <= R: vlo (the smallest stored column) is an admissible start of the bracket.
-  const int lane = threadIdx.x & 31;
-  while (vhi > vlo) {
-    const int64_t span = vhi - vlo;
-    int64_t v = (span <= 32) ? vlo + lane + 1 : vlo + (((int64_t)(lane + 1) * span + 31) >> 5);
-    if (v > vhi) v = vhi;
-    int64_t lb[NACHO_MAX_K];
-    int64_t cnt = 0;
-#pragma unroll
-    for (int o = 0; o < NACHO_MAX_K; ++o) {
-      if (o < k) {
-        lb[o] = lb_search(a.op[o].crd, wlo[o], whi[o], v);
-        cnt += lb[o] - seg[o];
-      }
-    }
-    const unsigned m = __ballot_sync(kFull, cnt <= R);
-    if (m == 0) {
-      const int64_t v0 = __shfl_sync(kFull, v, 0);
-#pragma unroll
-      for (int o = 0; o < NACHO_MAX_K; ++o) if (o < k) whi[o] = __shfl_sync(kFull, lb[o], 0) - 1;
-      vhi = v0 - 1;
-      continue;
-    }
-    const int j = 31 - __clz(m);
-    const int jn = j < 31 ? j + 1 : 31;
-    const int64_t vj = __shfl_sync(kFull, v, j), vn = __shfl_sync(kFull, v, jn);
-#pragma unroll
-    for (int o = 0; o < NACHO_MAX_K; ++o) {
-      if (o < k) {
-        const int64_t lj = __shfl_sync(kFull, lb[o], j), ln = __shfl_sync(kFull, lb[o], jn);
-        wlo[o] = lj;
-        if (j < 31 && vn > vj) whi[o] = ln - 1;
-      }
-    }
-    vlo = vj;
-    if (j < 31 && vn > vj) vhi = vn - 1;
-  }
-  b.col = (int32_t)vlo;
-#pragma unroll
-  for (int o = 0; o < NACHO_MAX_K; ++o) if (o < k) b.pos[o] = wlo[o];
+  warp_kway_select(a, k, lo, hi, R, b);
   return b;
 }
 

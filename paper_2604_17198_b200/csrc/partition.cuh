@@ -8,7 +8,7 @@ namespace nacho {
 // (reading R1), interior boundaries by FindPartition (Alg. 1).  The P+1 searches are independent
 // ("computed independently, and thus in parallel").
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) partition_kernel(OpsArg a, PartsArg out, int64_t qstar) {
+__global__ void __launch_bounds__(WARPS * 32) partition_kernel(const __grid_constant__ OpsArg a, PartsArg out, int64_t qstar) {
   const int64_t p = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (p > out.P) return;  // warp-uniform
   Boundary b;

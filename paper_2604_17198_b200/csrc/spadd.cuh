@@ -127,7 +127,7 @@ __device__ __forceinline__ void load_boundary(const PartsArg& P, int k, int64_t 
 // A partition holding more than TILE entries is processed in chunks whose ends are found by the
 // same FindPartition search (the hierarchy of P:1089-1093 applied inside the partition).
 template <typename T, bool FILL, int THREADS, int TILE>
-__global__ void __launch_bounds__(THREADS, 2) spadd_kernel(SpaddArgs<T> a) {
+__global__ void __launch_bounds__(THREADS, 2) spadd_kernel(const __grid_constant__ SpaddArgs<T> a) {
   constexpr int SPT = TILE / THREADS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SpaddShared<THREADS>& sh = *reinterpret_cast<SpaddShared<THREADS>*>(smem_raw);

@@ -170,6 +170,17 @@ def _spadd_check(ops, P=None):
     assert np.array_equal(z_pos.cpu().numpy(), rp), "Z.pos"
     assert np.array_equal(z_crd.cpu().numpy(), rc), "Z.crd"
     assert np.array_equal(z_val.cpu().numpy().view(np.uint8), rv.view(np.uint8)), "Z.val bits"
+    # single-pass (look-back) variant, when the partitions fit its tile
+    qstar = sum(A.nnz for A in ops)
+    if -(-qstar // parts.P) + len(ops) - 1 <= 2048:
+        po = torch.full((parts.P + 1,), -1, dtype=torch.int64, device=DEV)
+        fz_pos, fz_crd, fz_val = N.spadd_k_fused(dops, parts, part_off=po)
+        n = int(fz_pos[-1].item())
+        assert n == len(rc)
+        assert np.array_equal(po.cpu().numpy(), np.concatenate([[0], np.cumsum(cnt)])), "fused part_off"
+        assert np.array_equal(fz_pos.cpu().numpy(), rp), "fused Z.pos"
+        assert np.array_equal(fz_crd[:n].cpu().numpy(), rc), "fused Z.crd"
+        assert np.array_equal(fz_val[:n].cpu().numpy().view(np.uint8), rv.view(np.uint8)), "fused Z.val bits"
 
 
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 8])
