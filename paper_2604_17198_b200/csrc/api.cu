@@ -11,6 +11,7 @@
 #include "spadd3.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
+#include "spmv2.cuh"
 
 using namespace nacho;
 
@@ -53,7 +54,7 @@ constexpr int kPartWarps = 4;
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-int64_t spmv_tile(int dtype) { return dtype == NACHO_F64 ? kSpmvThreads * kSpmvIptF64 : kSpmvThreads * kSpmvIptF32; }
+int64_t spmv_tile(int dtype) { (void)dtype; return kSvTileMax; }  // = spmv2 tile
 
 nacho_status check_matrix(const nacho_matrix* A, const char* name) {
   if (!A) return fail(NACHO_ERR_INVALID_ARG, "%s: null descriptor", name);
@@ -141,6 +142,10 @@ nacho_status check_parts(const nacho_parts* p, int32_t k) {
 
 nacho_status launch_partition(const nacho_matrix* ops, int32_t k, const PartsArg& pa, cudaStream_t st) {
   const OpsArg a = make_ops(ops, k);
+  if (k == 1) {
+    partition1_kernel<<<(unsigned)((int64_t(pa.P) + 256) / 256), 256, 0, st>>>(a, pa, total_cost(ops, k));
+    return launched("partition1_kernel");
+  }
   const int64_t nb = (int64_t(pa.P) + 1 + kPartWarps - 1) / kPartWarps;
   partition_kernel<kPartWarps><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, total_cost(ops, k));
   return launched("partition_kernel");
@@ -160,6 +165,7 @@ nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, 
   a.pos = A->pos; a.crd = A->crd; a.val = static_cast<const T*>(A->val);
   a.outer = A->format == NACHO_DCSR ? A->outer_crd : nullptr;
   a.nouter = A->nouter;
+  a.ncols = A->ncols;
   a.x = static_cast<const T*>(x); a.y = static_cast<T*>(y);
   a.dense_y = (A->format == NACHO_DCSR && dense_y) ? 1 : 0;
   a.P = pa.P; a.ppos = pa.pos; a.prow = pa.row_pos;
@@ -168,9 +174,22 @@ nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, 
   if (a.dense_y) {
     if (cudaMemsetAsync(y, 0, sizeof(T) * A->nrows, st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "memset y");
   }
-  if constexpr (sizeof(T) == 8) spmv_kernel<T, kSpmvThreads, kSpmvIptF64><<<pa.P, kSpmvThreads, 0, st>>>(a);
-  else spmv_kernel<T, kSpmvThreads, kSpmvIptF32><<<pa.P, kSpmvThreads, 0, st>>>(a);
-  NACHO_TRY(launched("spmv_kernel"));
+  const int64_t maxpart = (A->nnz + pa.P - 1) / pa.P;
+  if (maxpart <= kSvTileMax) {  // TMA-staged kernel (spmv2.cuh)
+    static bool configured = false;
+    const size_t smem = sv2_smem_bytes<T>();
+    if (!configured) {
+      if (cudaFuncSetAttribute(spmv2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(spmv2_kernel)");
+      configured = true;
+    }
+    spmv2_kernel<T><<<pa.P, kSvThreads, smem, st>>>(a);
+    NACHO_TRY(launched("spmv2_kernel"));
+  } else {
+    if constexpr (sizeof(T) == 8) spmv_kernel<T, kSpmvThreads, kSpmvIptF64><<<pa.P, kSpmvThreads, 0, st>>>(a);
+    else spmv_kernel<T, kSpmvThreads, kSpmvIptF32><<<pa.P, kSpmvThreads, 0, st>>>(a);
+    NACHO_TRY(launched("spmv_kernel"));
+  }
   const int64_t warps = (pa.P + 31) / 32;
   spmv_fixup_kernel<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
   return launched("spmv_fixup_kernel");

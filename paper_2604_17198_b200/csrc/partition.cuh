@@ -30,4 +30,37 @@ __global__ void __launch_bounds__(WARPS * 32) partition_kernel(const __grid_cons
   }
 }
 
+// One operand (SpMV, SpMM, DCSR SpMV): the cut is a plain position split (Listing 7 specialised to
+// a single compressed operand: pos = Q_p), so only the row level needs a search --
+// one thread per boundary, binary search for the largest outer position x with pos[x] <= Q_p.
+__global__ void __launch_bounds__(256) partition1_kernel(const __grid_constant__ OpsArg a, PartsArg out,
+                                                         int64_t qstar) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > out.P) return;
+  const OpView& A = a.op[0];
+  const int64_t Q = query_of(qstar, out.P, p);
+  int64_t row, rp, pos;
+  int32_t col = 0;
+  if (p == 0) {
+    row = 0; rp = 0; pos = 0;                                         // origin (R1)
+  } else if (p == out.P || Q >= A.nnz) {
+    row = a.nrows; rp = A.nouter; pos = A.nnz;                        // end (R1, R2)
+  } else {
+    int64_t lo = 0, hi = A.nouter;                                    // pos[lo] <= Q < pos[hi+1]
+    while (lo < hi) {
+      const int64_t m = lo + ((hi - lo + 1) >> 1);
+      if (ldg(A.pos + m) <= Q) lo = m; else hi = m - 1;
+    }
+    rp = lo;
+    row = A.outer ? (int64_t)ldg(A.outer + lo) : lo;
+    pos = Q;
+    col = ldg(A.crd + Q);
+  }
+  out.query[p] = Q;
+  out.row[p] = row;
+  out.row_pos[p] = rp;
+  out.col[p] = col;
+  out.pos[p] = pos;
+}
+
 }  // namespace nacho

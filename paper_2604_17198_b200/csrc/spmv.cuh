@@ -11,6 +11,7 @@ struct SpmvArgs {
   const T* val;
   const int32_t* outer;   // DCSR row coordinates (only used for a dense y)
   int64_t nouter;
+  int64_t ncols;
   const T* x;
   T* y;
   int32_t dense_y;        // DCSR: write y[outer[rp]] instead of y[rp]
