@@ -175,7 +175,7 @@ nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, 
     if (cudaMemsetAsync(y, 0, sizeof(T) * A->nrows, st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "memset y");
   }
   const int64_t maxpart = (A->nnz + pa.P - 1) / pa.P;
-  if (maxpart <= kSvTileMax) {  // TMA-staged kernel (spmv2.cuh)
+  if (maxpart <= kSvTileMax) {  // TMA-staged kernel, one CTA per partition (spmv2.cuh)
     static bool configured = false;
     const size_t smem = sv2_smem_bytes<T>();
     if (!configured) {
@@ -252,7 +252,18 @@ nacho_status launch_spmm(const SpmmArgs<T>& a, cudaStream_t st) {
 }
 
 template <typename T>
-nacho_status run_spmm(const SpmmArgs<T>& a, cudaStream_t st) {
+nacho_status run_spmm(const SpmmArgs<T>& a, cudaStream_t st, int64_t nnz) {
+  if constexpr (sizeof(T) == 4) {
+    const bool al = reinterpret_cast<uintptr_t>(a.B) % 16 == 0 && reinterpret_cast<uintptr_t>(a.C) % 16 == 0 &&
+                    a.ldb % 4 == 0 && a.ldc % 4 == 0;
+    if (a.nb == 64 && al && (nnz + a.P - 1) / a.P <= kSm2Tile) {  // eight-lane-group fast path
+      spmm64_kernel<<<a.P, 256, 0, st>>>(a);
+      NACHO_TRY(launched("spmm64_kernel"));
+      const int64_t warps = (a.P + 31) / 32;
+      spmm_fixup_kernel<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
+      return launched("spmm_fixup_kernel");
+    }
+  }
   const int cpl = a.nb <= 32 ? 1 : a.nb <= 64 ? 2 : a.nb <= 128 ? 4 : 8;
   const bool vec = (reinterpret_cast<uintptr_t>(a.B) % (cpl * sizeof(T)) == 0) && (a.ldb % cpl == 0);
   switch (cpl) {
@@ -482,12 +493,12 @@ nacho_status nacho_spmm(const nacho_matrix* A, const nacho_parts* parts, const v
     SpmmArgs<double> a{A->pos, A->crd, static_cast<const double*>(A->val), A->nrows, static_cast<const double*>(B), ldb,
                        nb, static_cast<double*>(C), ldc, pa.P, pa.pos, pa.row_pos,
                        reinterpret_cast<int64_t*>(c), reinterpret_cast<double*>(c + align_up(P * 8))};
-    return run_spmm<double>(a, st);
+    return run_spmm<double>(a, st, A->nnz);
   }
   SpmmArgs<float> a{A->pos, A->crd, static_cast<const float*>(A->val), A->nrows, static_cast<const float*>(B), ldb,
                     nb, static_cast<float*>(C), ldc, pa.P, pa.pos, pa.row_pos,
                     reinterpret_cast<int64_t*>(c), reinterpret_cast<float*>(c + align_up(P * 8))};
-  return run_spmm<float>(a, st);
+  return run_spmm<float>(a, st, A->nnz);
 }
 
 nacho_status nacho_validate(const nacho_matrix* A, void* stream) {

@@ -103,17 +103,18 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_kernel(SpmmArgs<T> a) {
         int32_t mc = 0;
         T mv = T(0);
         if (lane < nn) { mc = ldg(a.crd + at + base + lane); mv = ldg(a.val + at + base + lane); }
-        for (int i = 0; i < nn; i += 4) {
-          T bb[4][CPL];
-          T vv[4];
+        constexpr int U = CPL <= 2 ? 8 : 4;  // B rows in flight per warp
+        for (int i = 0; i < nn; i += U) {
+          T bb[U][CPL];
+          T vv[U];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < U; ++u) {
             const int32_t c = __shfl_sync(kFull, mc, (i + u) & 31);
             vv[u] = __shfl_sync(kFull, mv, (i + u) & 31);
             if (i + u < nn) load_brow<T, CPL, VEC>(a, c, lane, bb[u]);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < U; ++u) {
             if (i + u < nn) {
               const int64_t q = at + base + i + u;
               while (next_end <= q) {
@@ -193,6 +194,128 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_kernel(SpmmArgs<T> a) {
   const bool has = s_ckey < a.nrows && s_ckey == rpE;
   if (tid == 0) a.carry_row[p] = has ? s_ckey : -1;
   for (int c = tid; c < a.nb; c += WARPS * 32) a.carry_val[(int64_t)p * a.nb + c] = has ? s_carry[c] : T(0);
+}
+
+// nb == 64 fp32 fast path: eight-lane groups, each lane owns 8 columns (two float4), so a warp
+// instruction advances four nonzeros (one per group) instead of one.  Group g of the CTA walks the
+// 32 consecutive positions [s + 32g, s + 32g + 32); heads, tails and the CTA carry combine across
+// the 32 groups in position order exactly like spmm_kernel's warps.
+constexpr int kSm2Groups = 32;       // 8-lane groups per CTA (256 threads)
+constexpr int kSm2Items = 32;        // positions per group
+constexpr int kSm2Tile = kSm2Groups * kSm2Items;
+
+__global__ void __launch_bounds__(256, 3) spmm64_kernel(const __grid_constant__ SpmmArgs<float> a) {
+  __shared__ float4 s_tail[kSm2Groups][16];   // 64 floats per group
+  __shared__ int64_t s_tkey[kSm2Groups];
+  const int tid = threadIdx.x, g = tid >> 3, gl = tid & 7;
+  const unsigned gmask = 0xffu << (tid & 24);
+  const int p = blockIdx.x;
+  const int64_t s = ldg(a.ppos + p), e = ldg(a.ppos + p + 1);
+  const int64_t rp0 = ldg(a.prow + p), rpE = ldg(a.prow + p + 1);
+  const int i0 = g * kSm2Items;
+  const int n = (int)(e - s);
+  const bool active = i0 < n || g == 0;
+  const int cnt = active ? max(0, min(kSm2Items, n - i0)) : 0;
+  const int64_t at = s + i0, bt = at + cnt;
+  float4 acc0 = make_float4(0, 0, 0, 0), acc1 = acc0, hv0 = acc0, hv1 = acc0;
+  bool head = true, head_done = false;
+  int64_t head_row = 0, rp = 0;
+  auto store_row = [&](int64_t r, const float4& u0, const float4& u1) {
+    float4* dst = reinterpret_cast<float4*>(a.C + r * a.ldc) + 2 * gl;
+    dst[0] = u0;
+    dst[1] = u1;
+  };
+  if (active) {
+    if (g == 0) {
+      rp = rp0;
+    } else {
+      int64_t lo = rp0, hi = rpE < a.nrows ? rpE : a.nrows;
+      while (lo < hi) {
+        const int64_t m = lo + ((hi - lo + 1) >> 1);
+        if (ldg(a.pos + m) <= at) lo = m; else hi = m - 1;
+      }
+      rp = lo;
+    }
+    int64_t next_end = rp < a.nrows ? ldg(a.pos + rp + 1) : INT64_MAX;
+    // the group's positions: lane gl holds positions gl, gl+8, gl+16, gl+24
+    int32_t mc[4];
+    float mv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = gl + 8 * u;
+      mc[u] = j < cnt ? ldg(a.crd + at + j) : 0;
+      mv[u] = j < cnt ? ldg(a.val + at + j) : 0.f;
+    }
+#pragma unroll
+    for (int ib = 0; ib < kSm2Items / 4; ++ib) {   // batches of 4 positions (static register indices)
+      if (4 * ib >= cnt) break;
+      float4 b0[4], b1[4];
+      float vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = 4 * ib + u;
+        const int32_t c = __shfl_sync(gmask, mc[j >> 3], j & 7, 8);
+        vv[u] = __shfl_sync(gmask, mv[j >> 3], j & 7, 8);
+        if (j < cnt) {
+          const float4* src = reinterpret_cast<const float4*>(a.B + (int64_t)c * a.ldb) + 2 * gl;
+          b0[u] = __ldg(src);
+          b1[u] = __ldg(src + 1);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = 4 * ib + u;
+        if (j < cnt) {
+          const int64_t q = at + j;
+          while (next_end <= q) {
+            if (head) { head_done = true; head_row = rp; hv0 = acc0; hv1 = acc1; head = false; }
+            else store_row(rp, acc0, acc1);
+            acc0 = make_float4(0, 0, 0, 0); acc1 = acc0;
+            ++rp;
+            next_end = ldg(a.pos + rp + 1);
+          }
+          const float v = vv[u];
+          acc0.x += v * b0[u].x; acc0.y += v * b0[u].y; acc0.z += v * b0[u].z; acc0.w += v * b0[u].w;
+          acc1.x += v * b1[u].x; acc1.y += v * b1[u].y; acc1.z += v * b1[u].z; acc1.w += v * b1[u].w;
+        }
+      }
+    }
+    while (rp < a.nrows && next_end <= bt) {
+      if (head) { head_done = true; head_row = rp; hv0 = acc0; hv1 = acc1; head = false; }
+      else store_row(rp, acc0, acc1);
+      acc0 = make_float4(0, 0, 0, 0); acc1 = acc0;
+      ++rp;
+      next_end = rp < a.nrows ? ldg(a.pos + rp + 1) : INT64_MAX;
+    }
+  }
+  if (gl == 0) s_tkey[g] = active ? rp : INT64_MAX;
+  s_tail[g][2 * gl] = acc0;
+  s_tail[g][2 * gl + 1] = acc1;
+  __syncthreads();
+  auto add4 = [](float4& x, const float4& y) { x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w; };
+  if (head_done) {  // carry into my head row: tails of the run of preceding groups with that key
+    float4 c0 = hv0, c1 = hv1;
+    for (int gg = g - 1; gg >= 0 && s_tkey[gg] == head_row; --gg) {
+      add4(c0, s_tail[gg][2 * gl]);
+      add4(c1, s_tail[gg][2 * gl + 1]);
+    }
+    store_row(head_row, c0, c1);
+  }
+  // CTA carry: the last active group's tail plus the run of groups before it with the same key
+  const int lastg = n > 0 ? (n - 1) / kSm2Items : 0;
+  if (g == lastg) {
+    const int64_t key = s_tkey[lastg];
+    float4 c0 = acc0, c1 = acc1;
+    for (int gg = lastg - 1; gg >= 0 && s_tkey[gg] == key; --gg) {
+      add4(c0, s_tail[gg][2 * gl]);
+      add4(c1, s_tail[gg][2 * gl + 1]);
+    }
+    const bool has = key < a.nrows && key == rpE;
+    if (gl == 0) a.carry_row[p] = has ? key : -1;
+    float4* dst = reinterpret_cast<float4*>(a.carry_val + (int64_t)p * 64) + 2 * gl;
+    dst[0] = has ? c0 : make_float4(0, 0, 0, 0);
+    dst[1] = has ? c1 : make_float4(0, 0, 0, 0);
+  }
 }
 
 template <typename T>

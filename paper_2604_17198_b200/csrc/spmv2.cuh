@@ -49,7 +49,7 @@ struct Sv2Shared {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kSvThreads, 3) spmv2_kernel(const __grid_constant__ SpmvArgs<T> a) {
+__global__ void __launch_bounds__(kSvThreads, 5) spmv2_kernel(const __grid_constant__ SpmvArgs<T> a) {
   constexpr int XCAP = Sv2Cfg<T>::XCAP;
   constexpr int W = kSvThreads / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
