@@ -158,6 +158,21 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
         P = N.auto_partitions(ops, "spadd")
     parts = N.Parts(P, k, ops[0].pos.device)
     local = parts if world == 1 else dist.slice_parts(parts, rank * P_l, (rank + 1) * P_l)
+    if world > 1:
+        def step_dist(timed=False):
+            m = [ev(torch)] if timed else None
+            N.partition(ops, P, out=parts)
+            if timed:
+                m.append(ev(torch))
+            dist.spadd(ops, parts)          # local single-pass SpAdd + NCCL all-gather of the Z segments
+            if timed:
+                m.append(ev(torch))
+            return m
+        times, sec = timer.run(step_dist, args.steps, args.warmup, ["partition", "spadd_fused+exchange"], soak_s=1.0)
+        vs = ops[0].val.element_size()
+        return dict(work=qstar, times=times, sec=sec, launches=5, algo_step=0, nnz_z=0, P=P,
+                    kernel_bytes={"spadd_fused+exchange": sum(n * (4 + vs) for n in nnz), "partition": 1},
+                    two_pass={}, dtype="f32" if vs == 4 else "f64", wl=wl, parts=parts)
     part_off = torch.empty(local.P + 1, dtype=torch.int64, device="cuda")
     ws = torch.empty(8 * (local.P + 64), dtype=torch.uint8, device="cuda")
     z_pos = torch.empty(M + 1, dtype=torch.int64, device="cuda")

@@ -132,6 +132,8 @@ PartsArg parts_arg(const nacho_parts* p) {
   return pa;
 }
 
+int64_t max_part_work(const nacho_matrix* ops, int32_t k, const PartsArg& pa, int64_t limit, cudaStream_t st);
+
 nacho_status check_parts(const nacho_parts* p, int32_t k) {
   if (!p) return fail(NACHO_ERR_INVALID_ARG, "null parts");
   if (p->P < 1) return fail(NACHO_ERR_INVALID_ARG, "parts.P = %d < 1", p->P);
@@ -174,7 +176,7 @@ nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, 
   if (a.dense_y) {
     if (cudaMemsetAsync(y, 0, sizeof(T) * A->nrows, st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "memset y");
   }
-  const int64_t maxpart = (A->nnz + pa.P - 1) / pa.P;
+  const int64_t maxpart = max_part_work(A, 1, pa, kSvTileMax, st);
   if (maxpart <= kSvTileMax) {  // TMA-staged kernel, one CTA per partition (spmv2.cuh)
     static bool configured = false;
     const size_t smem = sv2_smem_bytes<T>();
@@ -237,9 +239,24 @@ nacho_status launch_spadd2(const Spadd2Args<T>& a, cudaStream_t st) {
 }
 
 // Largest possible partition of a k-operand partition with P parts (Theorem 1 slack k-1).
-bool fits_sa_tile(const nacho_matrix* ops, int32_t k, int32_t P) {
+// Upper bound of the work of one partition of a k-operand partition record: ceil(span/P) + k - 1
+// (Theorem 1 slack), span = Q* for a whole record.  A record that is a slice of a finer one (the
+// device cuts of dist.py) has a smaller span: when the cheap bound fails, the span is read from the
+// record's first and last query (a synchronising 16-byte copy).
+int64_t max_part_work(const nacho_matrix* ops, int32_t k, const PartsArg& pa, int64_t limit, cudaStream_t st) {
   const int64_t q = total_cost(ops, k);
-  return (q + P - 1) / P + (k - 1) <= kSaTile;
+  int64_t w = (q + pa.P - 1) / pa.P + (k - 1);
+  if (w <= limit || pa.P < 1) return w;
+  int64_t ends[2] = {0, q};
+  if (cudaMemcpyAsync(&ends[0], pa.query, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&ends[1], pa.query + pa.P, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return w;
+  return (ends[1] - ends[0] + pa.P - 1) / pa.P + (k - 1);
+}
+
+bool fits_sa_tile(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, cudaStream_t st) {
+  return max_part_work(ops, k, parts_arg(parts), kSaTile, st) <= kSaTile;
 }
 
 template <typename T, int CPL, bool VEC>
@@ -388,7 +405,7 @@ nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho
   if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t* cnt = static_cast<int64_t*>(ws);
-  if (fits_sa_tile(ops, k, parts->P)) {
+  if (fits_sa_tile(ops, k, parts, st)) {
     if (ops[0].dtype == NACHO_F64) {
       Spadd2Args<double> a{make_ops(ops, k), parts_arg(parts), cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
       NACHO_TRY((launch_spadd2<double, kCount>(a, st)));
@@ -416,7 +433,7 @@ nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_
   NACHO_TRY(check_parts(parts, k));
   if (!part_off || !z_pos) return fail(NACHO_ERR_INVALID_ARG, "null part_off / z_pos");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (fits_sa_tile(ops, k, parts->P)) {
+  if (fits_sa_tile(ops, k, parts, st)) {
     if (ops[0].dtype == NACHO_F64) {
       Spadd2Args<double> a{make_ops(ops, k), parts_arg(parts), nullptr, const_cast<int64_t*>(part_off), nullptr, nullptr, z_pos,
                            z_crd, static_cast<double*>(z_val)};
@@ -443,11 +460,11 @@ nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts
   NACHO_TRY(check_parts(parts, k));
   if (!z_pos) return fail(NACHO_ERR_INVALID_ARG, "null z_pos");
   if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
-  if (!fits_sa_tile(ops, k, parts->P))
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!fits_sa_tile(ops, k, parts, st))
     return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kSaTile);
   const size_t need = nacho_spadd_k_workspace_size(ops, k, parts->P);
   if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto* flags = static_cast<unsigned long long*>(ws);
   if (cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * (parts->P + 1), st) != cudaSuccess)
     return fail(NACHO_ERR_CUDA, "memset look-back flags");
