@@ -35,11 +35,24 @@ def details(rep):
 
 def raw(rep):
     rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
-    h = rows[0]
+    h, units = rows[0], dict(zip(rows[0], rows[1]))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3, "ms": 1e-3, "nsecond": 1e-9}
     out = {}
     for r in rows[2:]:
         d = dict(zip(h, r))
-        out[(d.get("ID"), d.get("Kernel Name", "")[:70])] = {k: d.get(k) for k in RAW if k in d}
+        vals = {}
+        for k in RAW:
+            if k not in d:
+                continue
+            u = units.get(k, "")
+            try:
+                v = float(d[k].replace(",", ""))
+            except ValueError:
+                vals[k] = d[k]
+                continue
+            vals[k] = v * scale[u] if u in scale else v   # bytes / seconds when a unit is given
+        out[(d.get("ID"), d.get("Kernel Name", "")[:70])] = vals
     return out
 
 
@@ -81,7 +94,22 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("--lines", type=int, default=25)
+    ap.add_argument("--traffic", nargs=2, metavar=("KEY", "KERNEL_REGEX"),
+                    help="record dram read+write bytes per launch of the matching kernels (summed over one "
+                         "step's launches) under KEY in profiles/traffic.json")
+    ap.add_argument("--launches", type=int, default=1, help="launches of the matched kernels per report")
     a = ap.parse_args()
+    if a.traffic:
+        import json, os, re
+        key, rx = a.traffic
+        tot = sum(v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for k, v in raw(a.rep).items()
+                  if re.search(rx, k[1]))
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "traffic.json")
+        tab = json.load(open(path)) if os.path.exists(path) else {}
+        tab[key] = tot / a.launches
+        json.dump(tab, open(path, "w"), indent=1, sort_keys=True)
+        print(key, tab[key])
+        return 0
     for k, v in details(a.rep).items():
         print(k)
         for m in KEYS:
