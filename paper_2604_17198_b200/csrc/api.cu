@@ -149,7 +149,11 @@ nacho_status launch_partition(const nacho_matrix* ops, int32_t k, const PartsArg
     return launched("partition1_kernel");
   }
   const int64_t nb = (int64_t(pa.P) + 1 + kPartWarps - 1) / kPartWarps;
-  partition_kernel<kPartWarps><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, total_cost(ops, k));
+  const int64_t q = total_cost(ops, k);
+  if (k == 2) partition_kernel<kPartWarps, 2><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q);
+  else if (k == 3) partition_kernel<kPartWarps, 3><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q);
+  else if (k == 4) partition_kernel<kPartWarps, 4><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q);
+  else partition_kernel<kPartWarps, NACHO_MAX_K><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q);
   return launched("partition_kernel");
 }
 

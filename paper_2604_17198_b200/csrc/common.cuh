@@ -107,12 +107,13 @@ __device__ __forceinline__ void set_origin(const OpsArg& a, Boundary& b) {
 
 // #lanes c in [0, n) (n <= 32) with v(c) < x, for a per-lane value v non-decreasing over lanes and a
 // per-lane query x (binary search over lanes with shuffles; all lanes execute every shuffle).
-__device__ __forceinline__ int lanes_less(int64_t v, int64_t x, int n) {
+template <typename V>
+__device__ __forceinline__ int lanes_less(V v, V x, int n) {
   int lo = 0, hi = n;
 #pragma unroll
   for (int it = 0; it < 6; ++it) {
     const int mid = (lo + hi) >> 1;
-    const int64_t vm = __shfl_sync(kFull, v, mid & 31);
+    const V vm = __shfl_sync(kFull, v, mid & 31);
     if (lo < hi) { if (vm < x) lo = mid + 1; else hi = mid; }
   }
   return lo;
@@ -127,34 +128,39 @@ __device__ __forceinline__ int lanes_less(int64_t v, int64_t x, int n) {
 // the other windows' samples; the bracket that provably contains v* becomes the new windows
 // (shrinking them ~33/(k+1)-fold).  Once every window holds <= 32 entries the answer is resolved
 // exactly with lane shuffles.
-__device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&lo)[NACHO_MAX_K],
-                                              int64_t (&hi)[NACHO_MAX_K], int64_t R, Boundary& b) {
+// KM: compile-time bound on k (register arrays sized KM).  Column values are int32 (crd < ncols <=
+// INT32_MAX), so INT32_MAX is a safe "past the window" value.
+template <int KM>
+__device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&lo)[KM], int64_t (&hi)[KM], int64_t R,
+                                              Boundary& b) {
   const int lane = threadIdx.x & 31;
-  constexpr int64_t INF = INT64_MAX;
+  constexpr int32_t INF = INT32_MAX;
   for (;;) {
     int m = 0;
     int64_t lmax = -1;
 #pragma unroll
-    for (int o = 0; o < NACHO_MAX_K; ++o)
+    for (int o = 0; o < KM; ++o)
       if (o < k && hi[o] - lo[o] > lmax) { lmax = hi[o] - lo[o]; m = o; }
     if (lmax <= 32) break;
-    int64_t sp[NACHO_MAX_K], u[NACHO_MAX_K];
+    int64_t sp[KM];
+    int32_t u[KM];
 #pragma unroll
-    for (int o = 0; o < NACHO_MAX_K; ++o) {
+    for (int o = 0; o < KM; ++o) {
       if (o < k) {
         const int64_t len = hi[o] - lo[o];
-        if (len > 0) { sp[o] = lo[o] + ((int64_t)(lane + 1) * len) / 33; u[o] = ldg(a.op[o].crd + sp[o]); }
+        if (len > 0) { sp[o] = lo[o] + ((int64_t)(lane + 1) * len) / 33; u[o] = (int32_t)ldg(a.op[o].crd + sp[o]); }
         else { sp[o] = lo[o]; u[o] = INF; }
       }
     }
-    int64_t cand = 0, own = 0, spm = 0;
+    int32_t cand = 0;
+    int64_t own = 0, spm = 0;
 #pragma unroll
-    for (int o = 0; o < NACHO_MAX_K; ++o)
+    for (int o = 0; o < KM; ++o)
       if (o == m) { cand = u[o]; spm = sp[o]; own = sp[o] - lo[o]; }
     int64_t L = own, U = own;
-    int64_t Lo[NACHO_MAX_K], Uo[NACHO_MAX_K];
+    int64_t Lo[KM], Uo[KM];
 #pragma unroll
-    for (int o = 0; o < NACHO_MAX_K; ++o) {
+    for (int o = 0; o < KM; ++o) {
       if (o < k) {
         const int64_t len = hi[o] - lo[o];
         const int j = lanes_less(u[o], cand, len > 0 ? 32 : 0);
@@ -171,7 +177,7 @@ __device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&
     const int ib = above ? __ffs(above) - 1 : 32;
     int64_t drop = 0;
 #pragma unroll
-    for (int o = 0; o < NACHO_MAX_K; ++o) {
+    for (int o = 0; o < KM; ++o) {
       if (o < k) {
         const int64_t la = __shfl_sync(kFull, o == m ? spm - lo[o] : Lo[o], ia >= 0 ? ia : 0);
         const int64_t ub = __shfl_sync(kFull, o == m ? spm - lo[o] : Uo[o], ib < 32 ? ib : 0);
@@ -185,18 +191,18 @@ __device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&
     R -= drop;
   }
   // ---- exact resolution: every window holds <= 32 entries, lane l holds entry l of each
-  int64_t e[NACHO_MAX_K];
+  int32_t e[KM];
 #pragma unroll
-  for (int o = 0; o < NACHO_MAX_K; ++o)
-    if (o < k) e[o] = (lane < hi[o] - lo[o]) ? (int64_t)ldg(a.op[o].crd + lo[o] + lane) : INF;
-  int64_t vstar = INF;
+  for (int o = 0; o < KM; ++o)
+    if (o < k) e[o] = (lane < hi[o] - lo[o]) ? (int32_t)ldg(a.op[o].crd + lo[o] + lane) : INF;
+  int32_t vstar = INF;
   bool found = false;
 #pragma unroll
-  for (int o = 0; o < NACHO_MAX_K; ++o) {
+  for (int o = 0; o < KM; ++o) {
     if (o < k) {
       int64_t less = 0, leq = 0;
 #pragma unroll
-      for (int o2 = 0; o2 < NACHO_MAX_K; ++o2) {
+      for (int o2 = 0; o2 < KM; ++o2) {
         if (o2 < k) {
           const int n2 = (int)(hi[o2] - lo[o2]);
           less += lanes_less(e[o2], e[o], n2);
@@ -208,9 +214,9 @@ __device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&
       if (hm && !found) { vstar = __shfl_sync(kFull, e[o], __ffs(hm) - 1); found = true; }
     }
   }
-  b.col = (int32_t)vstar;
+  b.col = vstar;
 #pragma unroll
-  for (int o = 0; o < NACHO_MAX_K; ++o)
+  for (int o = 0; o < KM; ++o)
     if (o < k) b.pos[o] = lo[o] + __popc(__ballot_sync(kFull, e[o] < vstar));
 }
 
@@ -221,6 +227,7 @@ __device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&
 // k operands -> the highest column v with sum_o (lb_o(v) - seg_o) <= R, found by a 32-ary search
 // over column values in which every lane runs the per-operand lb_search of Listing 7 inside windows
 // that narrow round by round.
+template <int KM = NACHO_MAX_K>
 __device__ __noinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t Q, int64_t outer_lo, int64_t outer_hi) {
   Boundary b;
   const int k = a.k;
@@ -228,7 +235,7 @@ __device__ __noinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t Q, 
   auto outer_ok = [&](int64_t x) {
     int64_t s = 0;
 #pragma unroll
-    for (int o = 0; o < NACHO_MAX_K; ++o) if (o < k) s += ldg(a.op[o].pos + x);
+    for (int o = 0; o < KM; ++o) if (o < k) s += ldg(a.op[o].pos + x);
     return s <= Q;
   };
   const int64_t x = warp_highest_true(outer_lo, outer_hi, outer_ok);
@@ -241,17 +248,17 @@ __device__ __noinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t Q, 
     return b;
   }
   // ---- level j: the (R+1)-th smallest column of the multiset union of the row's k segments
-  int64_t lo[NACHO_MAX_K], hi[NACHO_MAX_K];
+  int64_t lo[KM], hi[KM];
   int64_t R = Q;
 #pragma unroll
-  for (int o = 0; o < NACHO_MAX_K; ++o) {
+  for (int o = 0; o < KM; ++o) {
     if (o < k) {
       lo[o] = ldg(a.op[o].pos + x);
       hi[o] = ldg(a.op[o].pos + x + 1);
       R -= lo[o];
     }
   }
-  warp_kway_select(a, k, lo, hi, R, b);
+  warp_kway_select<KM>(a, k, lo, hi, R, b);
   return b;
 }
 

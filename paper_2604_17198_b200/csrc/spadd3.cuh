@@ -274,17 +274,12 @@ struct SaSrc {
   __device__ __forceinline__ T val(int i) const { return v[ix(i)]; }
 };
 
-// Plain merge path Z = merge(X, Y) keeping duplicates; ties take X first, so equal keys stay in
-// operand order.  X[nx] and Y[ny] are all-ones sentinels.  Z (padded) gets its sentinel at nx + ny.
-template <typename T, bool VALS, typename KT, class SX, class SY>
-__device__ __forceinline__ void sa_pmerge(const SX& X, int nx, const SY& Y, int ny, KT* __restrict__ Z,
-                                          T* __restrict__ Zv) {
-  const int tid = threadIdx.x;
-  const int total = nx + ny;
-  const int d0 = min(total, tid * kSaSpt);
-  const int d1 = min(total, d0 + kSaSpt);
+// Merge-path split of diagonal d0 of merge(X, Y) (ties take X first): the number of X entries among
+// the first d0 merged ones.  4-ary steps (three independent probes per round).
+template <class SX, class SY>
+__device__ __forceinline__ int sa_split(const SX& X, int nx, const SY& Y, int ny, int d0) {
   int lo = max(0, d0 - ny), hi = min(d0, nx);
-  while (lo < hi) {  // 4-ary steps: three independent probes per round
+  while (lo < hi) {
     const int q1 = lo + ((hi - lo) >> 2), q2 = lo + ((hi - lo) >> 1), q3 = lo + 3 * ((hi - lo) >> 2);
     const bool c1 = X.key(q1) <= Y.key(d0 - 1 - q1);
     const bool c2 = X.key(q2) <= Y.key(d0 - 1 - q2);
@@ -294,53 +289,95 @@ __device__ __forceinline__ void sa_pmerge(const SX& X, int nx, const SY& Y, int 
     else if (c1) { lo = q1 + 1; hi = q2; }
     else hi = q1;
   }
-  int i = lo, j = d0 - lo;
+  return lo;
+}
+
+// One merge step: consumes the smaller head (X on ties), returns its key (and value), and refills
+// the consumed head with a single shared-memory load.
+template <typename T, bool VALS, typename KT, class SX, class SY>
+__device__ __forceinline__ KT sa_step(const SX& X, const SY& Y, int& i, int& j, KT& xk, KT& yk, T& v) {
+  const bool tx = xk <= yk;
+  const KT key = tx ? xk : yk;
+  if (VALS) v = *(tx ? X.v + X.ix(i) : Y.v + Y.ix(j));
+  i += tx ? 1 : 0;
+  j += tx ? 0 : 1;
+  const KT nk = *(tx ? X.k + X.ix(i) : Y.k + Y.ix(j));
+  xk = tx ? nk : xk;
+  yk = tx ? yk : nk;
+  return key;
+}
+
+// Plain merge path Z = merge(X, Y) keeping duplicates; ties take X first, so equal keys stay in
+// operand order.  X[nx] and Y[ny] are all-ones sentinels.  Z (padded) gets its sentinel at nx + ny.
+template <typename T, bool VALS, typename KT, class SX, class SY>
+__device__ __forceinline__ void sa_pmerge(const SX& X, int nx, const SY& Y, int ny, KT* __restrict__ Z,
+                                          T* __restrict__ Zv) {
+  const int tid = threadIdx.x;
+  const int total = nx + ny;
+  const int d0 = min(total, tid * kSaSpt);
+  const int d1 = min(total, d0 + kSaSpt);
+  int i = sa_split(X, nx, Y, ny, d0), j = d0 - i;
   KT xk = X.key(i), yk = Y.key(j);
 #pragma unroll
   for (int s = 0; s < kSaSpt; ++s) {
     if (d0 + s < d1) {
-      const bool tx = xk <= yk;
+      T v;
       const int zi = pd<KT>(d0 + s);
-      Z[zi] = tx ? xk : yk;
-      if (VALS) Zv[zi] = tx ? X.val(i) : Y.val(j);
-      i += tx ? 1 : 0;
-      j += tx ? 0 : 1;
-      xk = X.key(i);
-      yk = Y.key(j);
+      Z[zi] = sa_step<T, VALS>(X, Y, i, j, xk, yk, v);
+      if (VALS) Zv[zi] = v;
     }
   }
   if (d0 < d1 && d1 == total) Z[pd<KT>(total)] = ~KT(0);
   if (total == 0 && tid == 0) Z[pd<KT>(0)] = ~KT(0);
 }
 
-// Fold each run of equal keys of the merged sequence M (n entries, padded) left to right (R9),
-// compact the runs into U (padded); returns the union size.
-template <typename T, bool VALS, typename KT>
-__device__ __forceinline__ int sa_dedup(const KT* __restrict__ Mk, const T* __restrict__ Mv, int n,
-                                        KT* __restrict__ Uk, T* __restrict__ Uv, int64_t* red) {
+// The last merge stage fused with the fold: merges the diagonal range [d0, d1) of merge(X, Y) in
+// registers and folds every run of equal keys left to right in operand order (R9).  A run belongs to
+// the thread holding its first entry; that thread reads past d1 while the run continues (a run has
+// <= k entries, one per operand, so it never spans more than the next thread's range).  The runs are
+// compacted into U (padded) with one block scan; returns the union size.
+template <typename T, bool VALS, typename KT, class SX, class SY>
+__device__ __forceinline__ int sa_pmerge_fold(const SX& X, int nx, const SY& Y, int ny, KT* __restrict__ Uk,
+                                              T* __restrict__ Uv, int64_t* red) {
   const int tid = threadIdx.x;
-  const int d0 = min(n, tid * kSaSpt), d1 = min(n, d0 + kSaSpt);
+  const int total = nx + ny;
+  const int d0 = min(total, tid * kSaSpt);
+  const int d1 = min(total, d0 + kSaSpt);
+  int i = sa_split(X, nx, Y, ny, d0), j = d0 - i;
+  KT xk = X.key(i), yk = Y.key(j);
+  KT prev = ~KT(0);  // key of merged entry d0 - 1 (all-ones: none; never a key)
+  if (d0 > 0) {
+    const KT xp = i > 0 ? X.key(i - 1) : KT(0), yp = j > 0 ? Y.key(j - 1) : KT(0);
+    prev = xp > yp ? xp : yp;
+  }
   KT ok[kSaSpt];
   T ov[kSaSpt];
   unsigned em = 0;
-  KT prev = d0 > 0 ? Mk[pd<KT>(d0 - 1)] : ~KT(0);
+  bool mine = false;
+  T acc = T(0);
 #pragma unroll
   for (int s = 0; s < kSaSpt; ++s) {
     if (d0 + s < d1) {
-      const int i = d0 + s;
-      const KT key = Mk[pd<KT>(i)];
-      const bool first = key != prev;
+      T v;
+      const KT key = sa_step<T, VALS>(X, Y, i, j, xk, yk, v);
+      const bool fresh = key != prev;
+      mine = fresh || mine;
+      if (VALS) acc = fresh ? v : acc + v;
       prev = key;
-      if (first) {
-        ok[s] = key;
-        if (VALS) {
-          T v = Mv[pd<KT>(i)];
-          for (int t = i + 1; t < n && Mk[pd<KT>(t)] == key; ++t) v = v + Mv[pd<KT>(t)];
-          ov[s] = v;
-        }
-        em |= 1u << s;
-      }
+      ok[s] = key;
+      if (VALS) ov[s] = acc;
+      const KT nxt = xk < yk ? xk : yk;
+      if (mine && nxt != key) em |= 1u << s;
     }
+  }
+  if (d1 - d0 == kSaSpt && mine && (xk < yk ? xk : yk) == prev) {
+    while ((xk < yk ? xk : yk) == prev) {  // finish my last run past d1
+      T v;
+      sa_step<T, VALS>(X, Y, i, j, xk, yk, v);
+      if (VALS) acc = acc + v;
+    }
+    if (VALS) ov[kSaSpt - 1] = acc;
+    em |= 1u << (kSaSpt - 1);
   }
   int64_t tot;
   int64_t idx = sa_excl_sum((int64_t)__popc(em), red, &tot);
@@ -365,19 +402,26 @@ __device__ __forceinline__ int sa_union(SaShared<T>& sh, int k, const int* cs, c
     *upad = false;
     return ce[0] - cs[0];
   }
+  if (k == 2) {
+    *upad = true;
+    *Uk = B1;
+    *Uv = V1;
+    return sa_pmerge_fold<T, VALS, KT>(opsrc(0), ce[0] - cs[0], opsrc(1), ce[1] - cs[1], B1, V1, sh.red);
+  }
   int n = (ce[0] - cs[0]) + (ce[1] - cs[1]);
   sa_pmerge<T, VALS, KT>(opsrc(0), ce[0] - cs[0], opsrc(1), ce[1] - cs[1], B1, V1);
   __syncthreads();
   KT* Xk = B1; T* Xv = V1;
   KT* Dk = B2; T* Dv = V2;
-  for (int o = 2; o < k; ++o) {
+  for (int o = 2; o < k - 1; ++o) {
     sa_pmerge<T, VALS, KT>(SaSrc<KT, T, true>{Xk, Xv}, n, opsrc(o), ce[o] - cs[o], Dk, Dv);
     __syncthreads();
     n += ce[o] - cs[o];
     KT* tk = Xk; Xk = Dk; Dk = tk;
     T* tv = Xv; Xv = Dv; Dv = tv;
   }
-  const int nu = sa_dedup<T, VALS, KT>(Xk, Xv, n, Dk, Dv, sh.red);
+  const int nu = sa_pmerge_fold<T, VALS, KT>(SaSrc<KT, T, true>{Xk, Xv}, n, opsrc(k - 1), ce[k - 1] - cs[k - 1], Dk,
+                                             Dv, sh.red);
   *Uk = Dk;
   *Uv = Dv;
   *upad = true;
