@@ -11,7 +11,7 @@
 #include "spadd3.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
-#include "spmv2.cuh"
+#include "spmv3.cuh"
 
 using namespace nacho;
 
@@ -54,7 +54,7 @@ constexpr int kPartWarps = 4;
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-int64_t spmv_tile(int dtype) { (void)dtype; return kSvTileMax; }  // = spmv2 tile
+int64_t spmv_tile(int dtype) { return dtype == NACHO_F64 ? sv3_tile<double>() : sv3_tile<float>(); }  // = spmv3 tile
 
 nacho_status check_matrix(const nacho_matrix* A, const char* name) {
   if (!A) return fail(NACHO_ERR_INVALID_ARG, "%s: null descriptor", name);
@@ -180,17 +180,11 @@ nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, 
   if (a.dense_y) {
     if (cudaMemsetAsync(y, 0, sizeof(T) * A->nrows, st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "memset y");
   }
-  const int64_t maxpart = max_part_work(A, 1, pa, kSvTileMax, st);
-  if (maxpart <= kSvTileMax) {  // TMA-staged kernel, one CTA per partition (spmv2.cuh)
-    static bool configured = false;
-    const size_t smem = sv2_smem_bytes<T>();
-    if (!configured) {
-      if (cudaFuncSetAttribute(spmv2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(spmv2_kernel)");
-      configured = true;
-    }
-    spmv2_kernel<T><<<pa.P, kSvThreads, smem, st>>>(a);
-    NACHO_TRY(launched("spmv2_kernel"));
+  const int64_t maxpart = max_part_work(A, 1, pa, sv3_tile<T>(), st);
+  if (maxpart <= sv3_tile<T>()) {  // register-streaming kernel, one CTA per partition (spmv3.cuh)
+    if (a.dense_y) spmv3_kernel<T, true><<<pa.P, kSv3Threads, 0, st>>>(a);
+    else spmv3_kernel<T, false><<<pa.P, kSv3Threads, 0, st>>>(a);
+    NACHO_TRY(launched("spmv3_kernel"));
   } else {
     if constexpr (sizeof(T) == 8) spmv_kernel<T, kSpmvThreads, kSpmvIptF64><<<pa.P, kSpmvThreads, 0, st>>>(a);
     else spmv_kernel<T, kSpmvThreads, kSpmvIptF32><<<pa.P, kSpmvThreads, 0, st>>>(a);
