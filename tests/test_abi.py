@@ -45,8 +45,9 @@ def _desc(nnz, dtype=0, nrows=100, ncols=100):
 def test_auto_partitions_and_workspace_host_only():
     import paper_2604_17198_b200 as N
     L = N.lib
-    for nnz, dt, tile in [(0, 0, 2040), (1, 0, 2040), (2040, 0, 2040), (2041, 0, 2040), (10**9, 0, 2040),
-                          (5000, 1, 2040)]:
+    # SpMV tiles: 256 threads x 16 (fp32) / x 8 (fp64) positions per partition
+    for nnz, dt, tile in [(0, 0, 4096), (1, 0, 4096), (4096, 0, 4096), (4097, 0, 4096), (10**9, 0, 4096),
+                          (5000, 1, 2048)]:
         m = _desc(nnz, dt)
         assert L.nacho_auto_partitions(ctypes.byref(m), 1, 0) == max(1, -(-nnz // tile))
     ops = (N.Matrix * 3)(*[_desc(10**7) for _ in range(3)])
