@@ -58,6 +58,9 @@ def _load():
     L.nacho_spadd_k_count.argtypes = [vp, i32, vp, vp, vp, sz, vp]
     L.nacho_spadd_k_fill.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]
     L.nacho_spadd_k.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_spadd_k_staged.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_spadd_k_staged_workspace_size.argtypes = [vp, i32, i32]
+    L.nacho_spadd_k_staged_workspace_size.restype = sz
     L.nacho_spmm_workspace_size.argtypes = [vp, i32, i32]
     L.nacho_spmm_workspace_size.restype = sz
     L.nacho_spmm.argtypes = [vp, vp, vp, i64, i32, vp, i64, vp, sz, vp]
@@ -72,6 +75,7 @@ lib = _load()
 
 EXPORTS = ["nacho_partition", "nacho_auto_partitions", "nacho_spmv_workspace_size", "nacho_spmv",
            "nacho_spadd_k_workspace_size", "nacho_spadd_k_count", "nacho_spadd_k_fill", "nacho_spadd_k",
+           "nacho_spadd_k_staged_workspace_size", "nacho_spadd_k_staged",
            "nacho_spmm_workspace_size", "nacho_spmm", "nacho_validate", "nacho_last_error",
            "nacho_launch_count"]
 
@@ -228,6 +232,29 @@ def spadd_k_fused(ops, parts: Parts, z_pos=None, z_crd=None, z_val=None, part_of
     pc = parts.c()
     _check(lib.nacho_spadd_k(arr, len(ops), ctypes.byref(pc), _ptr(part_off), _ptr(z_pos), _ptr(z_crd), _ptr(z_val),
                              _ptr(ws), need, _stream(stream)))
+    return z_pos, z_crd, z_val
+
+
+def spadd_k_staged(ops, parts: Parts, z_pos=None, z_crd=None, z_val=None, part_off=None, ws=None, stream=None):
+    """nacho_spadd_k_staged: one read of the operands, no look-back (staged union -> scan -> placement).
+    Returns (z_pos, z_crd, z_val) with z_crd / z_val at capacity Q*; nnz_Z = z_pos[-1]."""
+    arr = _matrices(ops)
+    dev = ops[0].pos.device
+    cap = max(1, sum(int(A.crd.shape[0]) for A in ops))
+    if z_pos is None:
+        z_pos = torch.empty(ops[0].nrows + 1, dtype=torch.int64, device=dev)
+    if z_crd is None:
+        z_crd = torch.empty(cap, dtype=torch.int32, device=dev)
+    if z_val is None:
+        z_val = torch.empty(cap, dtype=ops[0].val.dtype, device=dev)
+    if part_off is None:
+        part_off = torch.empty(parts.P + 1, dtype=torch.int64, device=dev)
+    need = lib.nacho_spadd_k_staged_workspace_size(arr, len(ops), parts.P)
+    if ws is None or ws.numel() < need:
+        ws, _ = _workspace(need, dev)
+    pc = parts.c()
+    _check(lib.nacho_spadd_k_staged(arr, len(ops), ctypes.byref(pc), _ptr(part_off), _ptr(z_pos), _ptr(z_crd),
+                                    _ptr(z_val), _ptr(ws), need, _stream(stream)))
     return z_pos, z_crd, z_val
 
 

@@ -9,6 +9,7 @@
 #include "partition.cuh"
 #include "spadd.cuh"
 #include "spadd3.cuh"
+#include "spadd4.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
 #include "spmv3.cuh"
@@ -236,6 +237,21 @@ nacho_status launch_spadd2(const Spadd2Args<T>& a, cudaStream_t st) {
   return launched(MODE == kCount ? "spadd2_count" : MODE == kFill ? "spadd2_fill" : "spadd2_fused");
 }
 
+// One CTA per partition (spadd4.cuh); shared memory is dynamic (> 48 KB).
+template <typename T, int MODE>
+nacho_status launch_spadd4(const Spadd4Args<T>& a, cudaStream_t st) {
+  auto kern = spadd4_kernel<T, MODE>;
+  const size_t smem = sizeof(S4Shared<T>);
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(spadd4_kernel)");
+    configured = true;
+  }
+  kern<<<(unsigned)a.parts.P, kS4Threads, smem, st>>>(a);
+  return launched(MODE == kS4Count ? "spadd4_count" : MODE == kS4Fill ? "spadd4_fill" : MODE == kS4Fused ? "spadd4_fused" : "spadd4_stage");
+}
+
 // Largest possible partition of a k-operand partition with P parts (Theorem 1 slack k-1).
 // Upper bound of the work of one partition of a k-operand partition record: ceil(span/P) + k - 1
 // (Theorem 1 slack), span = Q* for a whole record.  A record that is a slice of a finer one (the
@@ -315,6 +331,22 @@ __global__ void validate_kernel(nacho_matrix A, int* flag) {
     }
   }
   if (bad) atomicMax(flag, bad);
+}
+
+template <typename T>
+nacho_status run_spadd_staged(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
+                              int64_t* z_pos, int32_t* z_crd, T* z_val, char* ws, cudaStream_t st) {
+  const int64_t q = total_cost(ops, k);
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws);
+  int32_t* t_crd = reinterpret_cast<int32_t*>(ws + align_up((size_t)(parts->P + 1) * 8));
+  T* t_val = reinterpret_cast<T*>(reinterpret_cast<char*>(t_crd) + align_up((size_t)q * 4));
+  Spadd4Args<T> a{make_ops(ops, k), parts_arg(parts), cnt, part_off, nullptr, nullptr, z_pos, t_crd, t_val};
+  NACHO_TRY((launch_spadd4<T, kS4Stage>(a, st)));
+  scan_counts_kernel<1024><<<1, 1024, 0, st>>>(cnt, parts->P, part_off);
+  NACHO_TRY(launched("scan_counts_kernel"));
+  Spadd4Args<T> c{make_ops(ops, k), parts_arg(parts), nullptr, part_off, nullptr, nullptr, z_pos, z_crd, z_val};
+  s4_compact_kernel<T><<<(unsigned)parts->P, kS4Threads, 0, st>>>(c, t_crd, t_val);
+  return launched("s4_compact_kernel");
 }
 
 }  // namespace
@@ -405,11 +437,11 @@ nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho
   int64_t* cnt = static_cast<int64_t*>(ws);
   if (fits_sa_tile(ops, k, parts, st)) {
     if (ops[0].dtype == NACHO_F64) {
-      Spadd2Args<double> a{make_ops(ops, k), parts_arg(parts), cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-      NACHO_TRY((launch_spadd2<double, kCount>(a, st)));
+      Spadd4Args<double> a{make_ops(ops, k), parts_arg(parts), cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+      NACHO_TRY((launch_spadd4<double, kS4Count>(a, st)));
     } else {
-      Spadd2Args<float> a{make_ops(ops, k), parts_arg(parts), cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-      NACHO_TRY((launch_spadd2<float, kCount>(a, st)));
+      Spadd4Args<float> a{make_ops(ops, k), parts_arg(parts), cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+      NACHO_TRY((launch_spadd4<float, kS4Count>(a, st)));
     }
   } else if (ops[0].dtype == NACHO_F64) {
     SpaddArgs<double> a{make_ops(ops, k), parts_arg(parts), total_cost(ops, k), cnt, nullptr, nullptr, nullptr, nullptr};
@@ -433,13 +465,13 @@ nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (fits_sa_tile(ops, k, parts, st)) {
     if (ops[0].dtype == NACHO_F64) {
-      Spadd2Args<double> a{make_ops(ops, k), parts_arg(parts), nullptr, const_cast<int64_t*>(part_off), nullptr, nullptr, z_pos,
-                           z_crd, static_cast<double*>(z_val)};
-      return launch_spadd2<double, kFill>(a, st);
+      Spadd4Args<double> a{make_ops(ops, k), parts_arg(parts), nullptr, const_cast<int64_t*>(part_off), nullptr, nullptr,
+                           z_pos, z_crd, static_cast<double*>(z_val)};
+      return launch_spadd4<double, kS4Fill>(a, st);
     }
-    Spadd2Args<float> a{make_ops(ops, k), parts_arg(parts), nullptr, const_cast<int64_t*>(part_off), nullptr, nullptr, z_pos,
-                        z_crd, static_cast<float*>(z_val)};
-    return launch_spadd2<float, kFill>(a, st);
+    Spadd4Args<float> a{make_ops(ops, k), parts_arg(parts), nullptr, const_cast<int64_t*>(part_off), nullptr, nullptr,
+                        z_pos, z_crd, static_cast<float*>(z_val)};
+    return launch_spadd4<float, kS4Fill>(a, st);
   }
   if (ops[0].dtype == NACHO_F64) {
     SpaddArgs<double> a{make_ops(ops, k), parts_arg(parts), total_cost(ops, k), nullptr, part_off, z_pos, z_crd,
@@ -467,13 +499,41 @@ nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts
   if (cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * (parts->P + 1), st) != cudaSuccess)
     return fail(NACHO_ERR_CUDA, "memset look-back flags");
   if (ops[0].dtype == NACHO_F64) {
-    Spadd2Args<double> a{make_ops(ops, k), parts_arg(parts), nullptr, part_off, flags, flags + parts->P, z_pos, z_crd,
+    Spadd4Args<double> a{make_ops(ops, k), parts_arg(parts), nullptr, part_off, flags, flags + parts->P, z_pos, z_crd,
                          static_cast<double*>(z_val)};
-    return launch_spadd2<double, kFused>(a, st);
+    return launch_spadd4<double, kS4Fused>(a, st);
   }
-  Spadd2Args<float> a{make_ops(ops, k), parts_arg(parts), nullptr, part_off, flags, flags + parts->P, z_pos, z_crd,
+  Spadd4Args<float> a{make_ops(ops, k), parts_arg(parts), nullptr, part_off, flags, flags + parts->P, z_pos, z_crd,
                       static_cast<float*>(z_val)};
-  return launch_spadd2<float, kFused>(a, st);
+  return launch_spadd4<float, kS4Fused>(a, st);
+}
+
+size_t nacho_spadd_k_staged_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {
+  if (!ops || k < 1) return 0;
+  const int64_t q = total_cost(ops, k);
+  const size_t vs = ops[0].dtype == NACHO_F64 ? 8 : 4;
+  return align_up((size_t)((P > 0 ? P : 1) + 1) * 8) + align_up((size_t)q * 4) + align_up((size_t)q * vs);
+}
+
+/* Single read of the operands, no look-back: staged union + scan + placement (spadd4.cuh). */
+nacho_status nacho_spadd_k_staged(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
+                                  int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  NACHO_TRY(check_ops(ops, k));
+  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands");
+  NACHO_TRY(check_parts(parts, k));
+  if (!z_pos || !part_off) return fail(NACHO_ERR_INVALID_ARG, "null z_pos / part_off");
+  if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!fits_sa_tile(ops, k, parts, st))
+    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kSaTile);
+  const size_t need = nacho_spadd_k_staged_workspace_size(ops, k, parts->P);
+  if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  if (ops[0].dtype == NACHO_F64)
+    return run_spadd_staged<double>(ops, k, parts, part_off, z_pos, z_crd, static_cast<double*>(z_val),
+                                    static_cast<char*>(ws), st);
+  return run_spadd_staged<float>(ops, k, parts, part_off, z_pos, z_crd, static_cast<float*>(z_val),
+                                 static_cast<char*>(ws), st);
 }
 
 size_t nacho_spmm_workspace_size(const nacho_matrix* A, int32_t P, int32_t nb) {

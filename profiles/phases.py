@@ -11,7 +11,7 @@ import torch  # noqa: E402
 import paper_2604_17198_b200 as N  # noqa: E402
 import workloads as W  # noqa: E402
 
-NAMES = ["stage_wait", "colrange", "keys", "union", "lookback", "output", "-", "-"]
+NAMES = ["ticket+bounds", "loads", "marks", "keys", "union", "offset", "writes", "-"]
 
 
 def main():
@@ -28,6 +28,7 @@ def main():
     buf = (ctypes.c_ulonglong * 16)()
     f = N.lib.nacho_debug_phases
     for it in range(3):
+        torch.cuda.synchronize()
         f(buf, 1)
         if mode == "fused":
             N.spadd_k_fused(ops, parts, zp, zc, zv, part_off=off)
@@ -36,9 +37,10 @@ def main():
         torch.cuda.synchronize()
     f(buf, 0)
     tot = sum(buf[i] for i in range(8)) or 1
-    print(mode, "CTA0 cycles:", tot, " per partition (~%d partitions):" % (P // 296))
+    ns = (P + 15) // 16   # sampled partitions (every 16th), one launch
+    print(mode, "sampled cycles:", tot, "per sampled partition: %.0f" % (tot / ns))
     for i, n in enumerate(NAMES):
-        print(f"  {n:10s} {buf[i]:>12d} {100 * buf[i] / tot:5.1f}%  {buf[i] / max(1, P // 296):9.0f} cyc/part")
+        print(f"  {n:14s} {buf[i]:>12d} {100 * buf[i] / tot:5.1f}%  {buf[i] / ns:9.0f} cyc/part")
 
 
 if __name__ == "__main__":

@@ -13,6 +13,8 @@ def t(fn, n=10):
     e0.record()
     for i in range(n): fn()
     e1.record(); torch.cuda.synchronize(); return e0.elapsed_time(e1)/n
-print(os.environ.get("NACHO_LIB"), "fused %.3f ms" % t(lambda: N.spadd_k_fused(ops, parts, zp, zc, zv, part_off=off)),
+ws = torch.empty(N.lib.nacho_spadd_k_staged_workspace_size(N._matrices(ops), len(ops), P), dtype=torch.uint8, device="cuda")
+print(os.environ.get("NACHO_LIB"), "staged %.3f ms" % t(lambda: N.spadd_k_staged(ops, parts, zp, zc, zv, part_off=off, ws=ws)),
+      "fused %.3f ms" % t(lambda: N.spadd_k_fused(ops, parts, zp, zc, zv, part_off=off)),
       "count %.3f ms" % t(lambda: N.spadd_k_count(ops, parts, off)), "fill %.3f" % t(lambda: N.spadd_k_fill(ops, parts, off, cap, zp, zc, zv)),
       "partition %.3f" % t(lambda: N.partition(ops, P, out=parts)))
