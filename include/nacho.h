@@ -133,6 +133,19 @@ size_t nacho_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t 
  *   ws  >= nacho_spadd_k_workspace_size(ops, k, P) bytes (look-back flags). */
 nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
                            int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes, void* stream);
+/* nacho_spadd_k_staged -- the same Z with one read of the operands and no look-back: every partition
+ * merges once and writes its union at the provisional offset sum_o b_p.pos[o] (an upper bound of its
+ * final offset, the cost C(b_p) of Theorem 1) of a workspace staging buffer, with
+ * partition-local Z.pos counts; an exclusive prefix sum of the union sizes and a placement
+ * pass then move every union to part_off[p] and add part_off[p] to the Z.pos entries it owns (R7).
+ *   part_off [P+1] int64 (required; part_off[P] = nnz_Z).  z_crd / z_val: capacity >= nnz_Z (Q* is
+ *   always enough).  Partitions must hold at most 2048 entries (as nacho_spadd_k).
+ *   ws  >= nacho_spadd_k_staged_workspace_size(ops, k, P) bytes: (P+1) int64 counts + Q* staged
+ *   (col, value) pairs.  Errors as nacho_spadd_k. */
+size_t nacho_spadd_k_staged_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P);
+nacho_status nacho_spadd_k_staged(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
+                                  int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes,
+                                  void* stream);
 nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
                                  void* ws, size_t ws_bytes, void* stream);
 nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_parts* parts,
