@@ -238,9 +238,9 @@ nacho_status launch_spadd2(const Spadd2Args<T>& a, cudaStream_t st) {
 }
 
 // One CTA per partition (spadd4.cuh); shared memory is dynamic (> 48 KB).
-template <typename T, int MODE>
-nacho_status launch_spadd4(const Spadd4Args<T>& a, cudaStream_t st) {
-  auto kern = spadd4_kernel<T, MODE>;
+template <typename T, int MODE, int KM>
+nacho_status launch_spadd4_k(const Spadd4Args<T>& a, cudaStream_t st) {
+  auto kern = spadd4_kernel<T, MODE, KM>;
   const size_t smem = sizeof(S4Shared<T>);
   static bool configured = false;
   if (!configured) {
@@ -250,6 +250,18 @@ nacho_status launch_spadd4(const Spadd4Args<T>& a, cudaStream_t st) {
   }
   kern<<<(unsigned)a.parts.P, kS4Threads, smem, st>>>(a);
   return launched(MODE == kS4Count ? "spadd4_count" : MODE == kS4Fill ? "spadd4_fill" : MODE == kS4Fused ? "spadd4_fused" : "spadd4_stage");
+}
+
+// One CTA per partition (spadd4.cuh); shared memory is dynamic (> 48 KB).  k = 2, 3 (and 1) get
+// compile-time operand loops; other k the generic instantiation.
+template <typename T, int MODE>
+nacho_status launch_spadd4(const Spadd4Args<T>& a, cudaStream_t st) {
+  switch (a.ops.k) {
+    case 1: return launch_spadd4_k<T, MODE, 1>(a, st);
+    case 2: return launch_spadd4_k<T, MODE, 2>(a, st);
+    case 3: return launch_spadd4_k<T, MODE, 3>(a, st);
+    default: return launch_spadd4_k<T, MODE, NACHO_MAX_K>(a, st);
+  }
 }
 
 // Largest possible partition of a k-operand partition with P parts (Theorem 1 slack k-1).

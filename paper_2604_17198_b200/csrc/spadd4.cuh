@@ -83,7 +83,7 @@ struct S4Shared {
   int32_t fred_f[kS4Threads / 32], fred_v[kS4Threads / 32];
   int32_t cmn[kS4Threads / 32], cmx[kS4Threads / 32];
   alignas(16) T val[kS4Tile];                     // operand values (concatenated)
-  alignas(16) int32_t col[kS4Tile];               // columns; 32-bit path: the operand keys in place
+  alignas(16) int32_t col[kS4Buf];                // columns (padded slots); 32-bit path: the keys in place
   alignas(16) uint32_t zk[2 * kS4Buf];            // 32-bit path: stage keys | 64-bit path: operand keys
   alignas(16) uint16_t zs[3 * kS4Buf];            // stage sources (2) + union sources
   alignas(16) T uv[kS4Buf];                       // union values; before that: the row marks
@@ -95,6 +95,14 @@ __device__ __forceinline__ void s4_mark_op(int& f, int& v, int f2, int v2) {
   f = f | f2;
 }
 
+// Merge input Y: operand keys, stored at padded slots of the concatenation (base = operand offset).
+template <typename KT>
+struct S4Y {
+  const KT* K;
+  int base;
+  __device__ __forceinline__ KT operator[](int j) const { return K[s4pd<KT>(base + j)]; }
+};
+
 // Merge input X: operand 0's keys (KIND 0, unpadded, source = index), a keyed stage buffer
 // (KIND 1: keys and sources at padded slots) or an index-only stage buffer (KIND 2: key = K[source]).
 template <typename KT, int KIND>
@@ -103,9 +111,9 @@ struct S4X {
   const KT* zk;
   const uint16_t* zs;
   __device__ __forceinline__ KT key(int i) const {
-    if constexpr (KIND == 0) return K[i];
+    if constexpr (KIND == 0) return K[s4pd<KT>(i)];
     else if constexpr (KIND == 1) return zk[s4pd<KT>(i)];
-    else return K[zs[s4pd<KT>(i)]];
+    else return K[s4pd<KT>(zs[s4pd<KT>(i)])];
   }
   __device__ __forceinline__ int src(int i) const {
     if constexpr (KIND == 0) return i;
@@ -115,7 +123,7 @@ struct S4X {
 
 // Merge-path split of diagonal d of merge(X, Y) (ties: X first): #X entries among the first d.
 template <typename KT, class XS>
-__device__ __forceinline__ int s4_split(const XS& X, int nx, const KT* Y, int ny, int d) {
+__device__ __forceinline__ int s4_split(const XS& X, int nx, const S4Y<KT>& Y, int ny, int d) {
   int lo = max(0, d - ny), hi = min(d, nx);
   while (lo < hi) {
     const int m = (lo + hi) >> 1;
@@ -127,7 +135,7 @@ __device__ __forceinline__ int s4_split(const XS& X, int nx, const KT* Y, int ny
 // One plain merge stage Z = merge(X, Y) keeping duplicates (ties: X first).  Y = an operand's keys,
 // sources ybase + j.  Z gets sources (and, if ZK, keys) at padded slots.
 template <typename KT, class XS>
-__device__ __forceinline__ void s4_merge(const XS& X, int nx, const KT* Y, int ybase, int ny, KT* ZK, uint16_t* ZS) {
+__device__ __forceinline__ void s4_merge(const XS& X, int nx, const S4Y<KT>& Y, int ybase, int ny, KT* ZK, uint16_t* ZS) {
   const int total = nx + ny;
   const int d0 = min(total, (int)threadIdx.x * kS4Vt), d1 = min(total, d0 + kS4Vt);
   if (d0 >= d1) return;
@@ -152,7 +160,7 @@ __device__ __forceinline__ void s4_merge(const XS& X, int nx, const KT* Y, int y
 // past its range while the run continues.  Writes the source of every run's first entry to US and
 // the folded value to UV (padded slots); returns the union size.
 template <typename T, typename KT, bool VALS, class XS>
-__device__ __forceinline__ int s4_merge_fold(const XS& X, int nx, const KT* Y, int ybase, int ny, const T* val,
+__device__ __forceinline__ int s4_merge_fold(const XS& X, int nx, const S4Y<KT>& Y, int ybase, int ny, const T* val,
                                              uint16_t* US, T* UV, int32_t* ired) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   constexpr KT INF = ~KT(0);
@@ -253,7 +261,7 @@ struct S4Out {
 // the rows it ends: run key -> row r0, the next merged key (the next union entry) -> row r1, rows
 // [r0, r1) end after this entry.  Rows before the first union entry are written by its emitter.
 template <typename T, typename KT, class XS>
-__device__ __forceinline__ int s4_merge_fold_emit(const XS& X, int nx, const KT* Y, int ybase, int ny, const T* val,
+__device__ __forceinline__ int s4_merge_fold_emit(const XS& X, int nx, const S4Y<KT>& Y, int ybase, int ny, const T* val,
                                                   int32_t* ired, const S4Out<T>& out) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   constexpr KT INF = ~KT(0);
@@ -332,15 +340,20 @@ __device__ __forceinline__ int s4_merge_fold_emit(const XS& X, int nx, const KT*
     if ((em >> s) & 1u) {
       out.z_crd[out.off + idx] = (int32_t)(ok[s] & cmask) + out.cmin;
       out.z_val[out.off + idx] = ov[s];
-      const int64_t r0 = (int64_t)(ok[s] >> out.cb);
-      int64_t r1 = nk[s] == INF ? out.L : (int64_t)(nk[s] >> out.cb);
-      r1 = r1 < out.L ? r1 : out.L;
+      // local rows fit 32 bits (key bits); L may not (trailing rows of the last partition)
+      const int r0 = (int)(ok[s] >> out.cb);
+      const int64_t r1 = nk[s] == INF ? out.L : min((int64_t)(nk[s] >> out.cb), out.L);
       if (first) {   // rows before the first union entry end empty
         const int64_t lead = r0 < out.L ? r0 : out.L;
         for (int64_t r = 0; r < lead; ++r) out.z_pos[out.row0 + r + 1] = out.pos_off;
         first = false;
       }
-      for (int64_t r = r0; r < r1; ++r) out.z_pos[out.row0 + r + 1] = out.pos_off + idx + 1;
+      if (r0 < r1) {
+        int64_t* zp = out.z_pos + out.row0 + 1;
+        const int64_t v = out.pos_off + idx + 1;
+        zp[r0] = v;
+        for (int64_t r = r0 + 1; r < r1; ++r) zp[r] = v;   // empty rows after it
+      }
       ++idx;
     }
   }
@@ -392,15 +405,15 @@ __device__ __forceinline__ int s4_union(S4Shared<T>& sh, int k, const KT* K, KT*
   const int* off = sh.off;
   if (k == 1) {
     const S4X<KT, 0> X{K, nullptr, nullptr};
-    return s4_merge_fold<T, KT, VALS>(X, off[1], K, 0, 0, sh.val, US, UV, sh.ired);
+    return s4_merge_fold<T, KT, VALS>(X, off[1], S4Y<KT>{K, 0}, 0, 0, sh.val, US, UV, sh.ired);
   }
   if (k == 2) {
     const S4X<KT, 0> X{K, nullptr, nullptr};
-    return s4_merge_fold<T, KT, VALS>(X, off[1], K + off[1], off[1], off[2] - off[1], sh.val, US, UV, sh.ired);
+    return s4_merge_fold<T, KT, VALS>(X, off[1], S4Y<KT>{K, off[1]}, off[1], off[2] - off[1], sh.val, US, UV, sh.ired);
   }
   {
     const S4X<KT, 0> X{K, nullptr, nullptr};
-    s4_merge<KT>(X, off[1], K + off[1], off[1], off[2] - off[1], KIND == 1 ? Z1 : nullptr, S1);
+    s4_merge<KT>(X, off[1], S4Y<KT>{K, off[1]}, off[1], off[2] - off[1], KIND == 1 ? Z1 : nullptr, S1);
   }
   __syncthreads();
   KT* xk = Z1;
@@ -409,13 +422,13 @@ __device__ __forceinline__ int s4_union(S4Shared<T>& sh, int k, const KT* K, KT*
   uint16_t* zs = S2;
   for (int o = 2; o < k - 1; ++o) {
     const S4X<KT, KIND> X{K, xk, xs};
-    s4_merge<KT>(X, off[o], K + off[o], off[o], off[o + 1] - off[o], KIND == 1 ? zk : nullptr, zs);
+    s4_merge<KT>(X, off[o], S4Y<KT>{K, off[o]}, off[o], off[o + 1] - off[o], KIND == 1 ? zk : nullptr, zs);
     __syncthreads();
     KT* tk = xk; xk = zk; zk = tk;
     uint16_t* ts = xs; xs = zs; zs = ts;
   }
   const S4X<KT, KIND> X{K, xk, xs};
-  return s4_merge_fold<T, KT, VALS>(X, off[k - 1], K + off[k - 1], off[k - 1], off[k] - off[k - 1], sh.val, US, UV,
+  return s4_merge_fold<T, KT, VALS>(X, off[k - 1], S4Y<KT>{K, off[k - 1]}, off[k - 1], off[k] - off[k - 1], sh.val, US, UV,
                                     sh.ired);
 }
 
@@ -427,11 +440,11 @@ __device__ __forceinline__ int s4_union_emit(S4Shared<T>& sh, int k, const KT* K
   if (k <= 2) {
     const S4X<KT, 0> X{K, nullptr, nullptr};
     const int ny = k == 2 ? off[2] - off[1] : 0;
-    return s4_merge_fold_emit<T, KT>(X, off[1], K + off[1], off[1], ny, sh.val, sh.ired, out);
+    return s4_merge_fold_emit<T, KT>(X, off[1], S4Y<KT>{K, off[1]}, off[1], ny, sh.val, sh.ired, out);
   }
   {
     const S4X<KT, 0> X{K, nullptr, nullptr};
-    s4_merge<KT>(X, off[1], K + off[1], off[1], off[2] - off[1], KIND == 1 ? Z1 : nullptr, S1);
+    s4_merge<KT>(X, off[1], S4Y<KT>{K, off[1]}, off[1], off[2] - off[1], KIND == 1 ? Z1 : nullptr, S1);
   }
   __syncthreads();
   KT* xk = Z1;
@@ -440,25 +453,25 @@ __device__ __forceinline__ int s4_union_emit(S4Shared<T>& sh, int k, const KT* K
   uint16_t* zs = S2;
   for (int o = 2; o < k - 1; ++o) {
     const S4X<KT, KIND> X{K, xk, xs};
-    s4_merge<KT>(X, off[o], K + off[o], off[o], off[o + 1] - off[o], KIND == 1 ? zk : nullptr, zs);
+    s4_merge<KT>(X, off[o], S4Y<KT>{K, off[o]}, off[o], off[o + 1] - off[o], KIND == 1 ? zk : nullptr, zs);
     __syncthreads();
     KT* tk = xk; xk = zk; zk = tk;
     uint16_t* ts = xs; xs = zs; zs = ts;
   }
   const S4X<KT, KIND> X{K, xk, xs};
-  return s4_merge_fold_emit<T, KT>(X, off[k - 1], K + off[k - 1], off[k - 1], off[k] - off[k - 1], sh.val, sh.ired,
+  return s4_merge_fold_emit<T, KT>(X, off[k - 1], S4Y<KT>{K, off[k - 1]}, off[k - 1], off[k] - off[k - 1], sh.val, sh.ired,
                                    out);
 }
 
 // Keys (32- or 64-bit), union, offset and writes of one partition.
-template <typename T, typename KT, int MODE>
+template <typename T, typename KT, int MODE, int KM>
 __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh, int64_t p, int n, int64_t row0,
                                         int64_t row1, int cb, int32_t cmin, unsigned long long& s4t) {
   (void)s4t;
   constexpr bool VALS = MODE != kS4Count;
   constexpr int KIND = sizeof(KT) == 4 ? 1 : 2;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int k = a.ops.k;
+  const int k = KM < NACHO_MAX_K ? KM : a.ops.k;
   const int32_t* mark = reinterpret_cast<const int32_t*>(sh.uv);
   KT* K = sizeof(KT) == 4 ? reinterpret_cast<KT*>(sh.col) : reinterpret_cast<KT*>(sh.zk);
 
@@ -470,7 +483,7 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh,
 #pragma unroll
     for (int s = 0; s < kS4Vt; ++s) {
       const int j = j0 + s;
-      mk[s] = j < n ? mark[j] : -1;
+      mk[s] = j < n ? mark[s4pd<uint32_t>(j)] : -1;
       s4_mark_op(f, v, mk[s] >= 0, mk[s]);
       mv[s] = v;
     }
@@ -494,7 +507,7 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh,
       if (j < n) {
         seen = seen || mk[s] >= 0;
         const int lr = seen ? mv[s] : pv;
-        K[j] = ((KT)(uint32_t)lr << cb) | (KT)(uint32_t)(sh.col[j] - cmin);
+        K[s4pd<KT>(j)] = ((KT)(uint32_t)lr << cb) | (KT)(uint32_t)(sh.col[s4pd<uint32_t>(j)] - cmin);
       }
     }
   }
@@ -521,7 +534,8 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh,
       out.pos_off = out.off;
     } else {
       out.off = 0;
-      for (int o = 0; o < k; ++o) out.off += sh.b0pos[o];   // provisional: sum_o b_p.pos[o] >= final
+#pragma unroll
+      for (int o = 0; o < KM; ++o) if (o < k) out.off += sh.b0pos[o];   // provisional: sum_o b_p.pos[o]
       out.pos_off = 0;
     }
     if (p == 0 && tid == 0) a.z_pos[0] = 0;
@@ -556,12 +570,12 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh,
   const KT cmask = (KT)(((KT)1 << cb) - 1);
   for (int j = tid; j < nu; j += kS4Threads) {
     const int src = US[s4pd<KT>(j)];
-    a.z_crd[off + j] = (int32_t)(K[src] & cmask) + cmin;
+    a.z_crd[off + j] = (int32_t)(K[s4pd<KT>(src)] & cmask) + cmin;
     a.z_val[off + j] = sh.uv[s4pd<KT>(j)];
   }
   const int64_t L = row1 - row0;
   if (p == 0 && tid == 0) a.z_pos[0] = 0;
-  auto row_of = [&](int j) -> int64_t { return (int64_t)(K[US[s4pd<KT>(j)]] >> cb); };
+  auto row_of = [&](int j) -> int64_t { return (int64_t)(K[s4pd<KT>(US[s4pd<KT>(j)])] >> cb); };
   {
     const int64_t lead = nu > 0 ? (row_of(0) < L ? row_of(0) : L) : L;   // rows before the first entry
     for (int64_t r = tid; r < lead; r += kS4Threads) a.z_pos[row0 + r + 1] = pos_off;
@@ -580,13 +594,14 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh,
   S4PH(6);
 }
 
-template <typename T, int MODE>
+// KM: compile-time operand count (1..4), or NACHO_MAX_K for any k (read from a.ops.k).
+template <typename T, int MODE, int KM>
 __global__ void __launch_bounds__(kS4Threads, 4) spadd4_kernel(const __grid_constant__ Spadd4Args<T> a) {
   constexpr bool VALS = MODE != kS4Count;
   extern __shared__ __align__(16) unsigned char s4raw[];
   S4Shared<T>& sh = *reinterpret_cast<S4Shared<T>*>(s4raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int k = a.ops.k;
+  const int k = KM < NACHO_MAX_K ? KM : a.ops.k;
   int64_t p;
   S4PH_INIT;
   if (MODE == kS4Fused) {
@@ -640,19 +655,19 @@ __global__ void __launch_bounds__(kS4Threads, 4) spadd4_kernel(const __grid_cons
   {
     int32_t c[kS4Vt];
     T v[kS4Vt];
-    int ob[NACHO_MAX_K - 1];   // concatenation offsets 1..7 (INT32_MAX past k): o(j) = #{ob <= j}
+    int ob[KM > 1 ? KM - 1 : 1];   // concatenation offsets 1..KM-1 (INT32_MAX past k): o(j) = #{ob <= j}
 #pragma unroll
-    for (int o = 0; o < NACHO_MAX_K - 1; ++o) ob[o] = sh.off[o + 1];
+    for (int o = 0; o < KM - 1; ++o) ob[o] = sh.off[o + 1];
 #pragma unroll
     for (int i = 0; i < kS4Vt; ++i) {
       const int j = tid + kS4Threads * i;
       if (j < n) {
         int o = 0;
 #pragma unroll
-        for (int oo = 0; oo < NACHO_MAX_K - 1; ++oo) o += j >= ob[oo] ? 1 : 0;
+        for (int oo = 0; oo < KM - 1; ++oo) o += j >= ob[oo] ? 1 : 0;
         c[i] = ldg(sh.crdp[o] + j);
         if (VALS) v[i] = ldg(reinterpret_cast<const T*>(sh.valp[o]) + j);
-        mark[j] = (j == sh.off[o]) ? 0 : -1;   // a range's first entry belongs to row0 unless marked
+        mark[s4pd<uint32_t>(j)] = (j == sh.off[o]) ? 0 : -1;   // a range's first entry belongs to row0 unless marked
       }
     }
     if (pre) {
@@ -665,7 +680,7 @@ __global__ void __launch_bounds__(kS4Threads, 4) spadd4_kernel(const __grid_cons
           const int f = tid + (half * kS4PosRound + m) * kS4Threads;
           int po = 0;
 #pragma unroll
-          for (int oo = 1; oo < NACHO_MAX_K; ++oo) po += (oo < k && f >= oo * np) ? 1 : 0;
+          for (int oo = 1; oo < KM; ++oo) po += (oo < k && f >= oo * np) ? 1 : 0;
           const int pi = f - po * np;
           pv[m] = f < k * np ? ldg(sh.posp[po] + pi) - sh.b0pos[po] : 0;
         }
@@ -680,7 +695,7 @@ __global__ void __launch_bounds__(kS4Threads, 4) spadd4_kernel(const __grid_cons
     for (int i = 0; i < kS4Vt; ++i) {
       const int j = tid + kS4Threads * i;
       if (j < n) {
-        sh.col[j] = c[i];
+        sh.col[s4pd<uint32_t>(j)] = c[i];
         if (VALS) sh.val[j] = v[i];
         cmn = min(cmn, c[i]);
         cmx = max(cmx, c[i]);
@@ -702,7 +717,7 @@ __global__ void __launch_bounds__(kS4Threads, 4) spadd4_kernel(const __grid_cons
       const int32_t* sp = spos + o * np;
       for (int r = tid; r < (int)span; r += kS4Threads) {
         const int ps = sp[r], pe = sp[r + 1];
-        if (ps < no && pe > ps) mark[base + ps] = r + 1;
+        if (ps < no && pe > ps) mark[s4pd<uint32_t>(base + ps)] = r + 1;
       }
     } else {
       const int64_t s = sh.b0pos[o];
@@ -710,7 +725,7 @@ __global__ void __launch_bounds__(kS4Threads, 4) spadd4_kernel(const __grid_cons
 #pragma unroll 2
       for (int64_t r = 1 + tid; r <= span; r += kS4Threads) {
         const int64_t ps = ldg(pos + r) - s, pe = ldg(pos + r + 1) - s;
-        if (ps >= 0 && ps < no && pe > ps) mark[base + (int)ps] = (int)r;
+        if (ps >= 0 && ps < no && pe > ps) mark[s4pd<uint32_t>(base + (int)ps)] = (int)r;
       }
     }
   }
@@ -722,8 +737,8 @@ __global__ void __launch_bounds__(kS4Threads, 4) spadd4_kernel(const __grid_cons
   S4PH(2);
   const int cb = 32 - __clz((unsigned)(cmax - cmin));                       // column bits (0 if one column)
   const int rb = span > 0 ? 64 - __clzll((unsigned long long)span) : 0;      // local row bits
-  if (rb + cb <= 31) s4_body<T, uint32_t, MODE>(a, sh, p, n, row0, row1, cb, cmin, s4t);
-  else s4_body<T, uint64_t, MODE>(a, sh, p, n, row0, row1, 32, cmin, s4t);
+  if (rb + cb <= 31) s4_body<T, uint32_t, MODE, KM>(a, sh, p, n, row0, row1, cb, cmin, s4t);
+  else s4_body<T, uint64_t, MODE, KM>(a, sh, p, n, row0, row1, 32, cmin, s4t);
 }
 
 // Places the staged unions (kS4Stage): partition p's union moves from its provisional offset
