@@ -8,7 +8,6 @@
 #include "common.cuh"
 #include "partition.cuh"
 #include "spadd.cuh"
-#include "spadd3.cuh"
 #include "spadd4.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
@@ -211,33 +210,6 @@ nacho_status launch_spadd(const SpaddArgs<T>& a, cudaStream_t st) {
   return launched(FILL ? "spadd_fill_kernel" : "spadd_count_kernel");
 }
 
-// Persistent warp-specialised SpAdd (spadd2.cuh): grid = resident CTAs (look-back needs them all
-// co-resident), each CTA walks partitions blockIdx.x, +gridDim.x, ...
-template <typename T, int MODE>
-nacho_status launch_spadd2(const Spadd2Args<T>& a, cudaStream_t st) {
-  auto kern = spadd2_kernel<T, MODE>;
-  const size_t smem = sa_smem_bytes<T>(a.ops.k, MODE != kCount);
-  static int occ = -1;
-  static size_t occ_smem = 0;
-  if (occ < 0 || occ_smem != smem) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(spadd2_kernel)");
-    int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kSaThreads, smem) != cudaSuccess || blocks < 1)
-      return fail(NACHO_ERR_CUDA, "spadd2_kernel does not fit an SM (%zu bytes of shared memory)", smem);
-    occ = blocks;
-    occ_smem = smem;
-  }
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t grid = (int64_t)sms * occ;
-  if (grid > a.parts.P) grid = a.parts.P;
-  kern<<<(unsigned)grid, kSaThreads, smem, st>>>(a);
-  return launched(MODE == kCount ? "spadd2_count" : MODE == kFill ? "spadd2_fill" : "spadd2_fused");
-}
-
-// One CTA per partition (spadd4.cuh); shared memory is dynamic (> 48 KB).
 template <typename T, int MODE, int KM>
 nacho_status launch_spadd4_k(const Spadd4Args<T>& a, cudaStream_t st) {
   auto kern = spadd4_kernel<T, MODE, KM>;
@@ -282,7 +254,7 @@ int64_t max_part_work(const nacho_matrix* ops, int32_t k, const PartsArg& pa, in
 }
 
 bool fits_sa_tile(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, cudaStream_t st) {
-  return max_part_work(ops, k, parts_arg(parts), kSaTile, st) <= kSaTile;
+  return max_part_work(ops, k, parts_arg(parts), kS4Tile, st) <= kS4Tile;
 }
 
 template <typename T, int CPL, bool VEC>
@@ -397,7 +369,7 @@ int32_t nacho_auto_partitions(const nacho_matrix* ops, int32_t k, int32_t op) {
   if (!ops || k < 1) return 1;
   const int64_t work = total_cost(ops, k);
   if (op == 0) return auto_p(work, spmv_tile(ops[0].dtype));
-  if (op == 1) return auto_p(work, kSpaddTile - (k - 1));
+  if (op == 1) return auto_p(work, kS4Tile - (k - 1));
   return auto_p(work, kSpmmWarps * kSpmmWitems);
 }
 
@@ -504,7 +476,7 @@ nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts
   if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (!fits_sa_tile(ops, k, parts, st))
-    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kSaTile);
+    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kS4Tile);
   const size_t need = nacho_spadd_k_workspace_size(ops, k, parts->P);
   if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   auto* flags = static_cast<unsigned long long*>(ws);
@@ -538,7 +510,7 @@ nacho_status nacho_spadd_k_staged(const nacho_matrix* ops, int32_t k, const nach
   if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (!fits_sa_tile(ops, k, parts, st))
-    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kSaTile);
+    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kS4Tile);
   const size_t need = nacho_spadd_k_staged_workspace_size(ops, k, parts->P);
   if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   if (ops[0].dtype == NACHO_F64)

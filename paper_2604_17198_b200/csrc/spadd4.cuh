@@ -31,6 +31,7 @@ enum S4Mode { kS4Count = 0, kS4Fill = 1, kS4Fused = 2, kS4Stage = 3 };
 
 // Phase timers (debug build -DNACHO_PROF): thread 0 of every 16th partition adds its clock64 deltas.
 #ifdef NACHO_PROF
+__device__ unsigned long long g_phase[16];
 #define S4PH(id)                                                           \
   do {                                                                     \
     if (threadIdx.x == 0 && (p & 15) == 0) {                               \
@@ -46,7 +47,13 @@ enum S4Mode { kS4Count = 0, kS4Fill = 1, kS4Fused = 2, kS4Stage = 3 };
 #endif
 
 constexpr int kS4Threads = 256;
-constexpr int kS4Vt = 8;                          // merged entries per thread and stage
+#ifndef NACHO_S4_VT   // tuning override
+#define NACHO_S4_VT 8
+#endif
+#ifndef NACHO_S4_MINB
+#define NACHO_S4_MINB 4
+#endif
+constexpr int kS4Vt = NACHO_S4_VT;                // merged entries per thread and stage
 constexpr int kS4Tile = kS4Threads * kS4Vt;       // entries per partition
 constexpr int kS4Buf = kS4Tile + kS4Tile / 16 + 8;   // padded stage-buffer capacity (elements)
 constexpr int kS4PosRound = 8;                    // row pointers loaded per thread and round
@@ -596,7 +603,7 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh,
 
 // KM: compile-time operand count (1..4), or NACHO_MAX_K for any k (read from a.ops.k).
 template <typename T, int MODE, int KM>
-__global__ void __launch_bounds__(kS4Threads, 4) spadd4_kernel(const __grid_constant__ Spadd4Args<T> a) {
+__global__ void __launch_bounds__(kS4Threads, NACHO_S4_MINB) spadd4_kernel(const __grid_constant__ Spadd4Args<T> a) {
   constexpr bool VALS = MODE != kS4Count;
   extern __shared__ __align__(16) unsigned char s4raw[];
   S4Shared<T>& sh = *reinterpret_cast<S4Shared<T>*>(s4raw);
