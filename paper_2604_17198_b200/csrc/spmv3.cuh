@@ -72,42 +72,15 @@ struct FV { int f; T v; };
 template <typename T>
 __device__ __forceinline__ FV<T> fv_op(FV<T> a, FV<T> b) { return FV<T>{a.f | b.f, b.f ? b.v : a.v + b.v}; }
 
-template <typename T, bool DY>
-__global__ void __launch_bounds__(kSv3Threads, Sv3Cfg<T>::MINB) spmv3_kernel(const __grid_constant__ SpmvArgs<T> a) {
-  constexpr int V = Sv3Cfg<T>::V;
-  constexpr int WCH = 32 * V;                  // positions per warp chunk
-  constexpr int SLOTS = kSv3Threads * V;
+// Steps 2-5 of a tile (after the products are in sprod and the row ends in send, and a barrier):
+// row-start marks, segmented scan, row sums, carry.  Ends with every smem read done (barrier).
+template <typename T, int V, bool DY>
+__device__ __forceinline__ void sv3_tail(const SpmvArgs<T>& a, int p, int64_t s, int n, int64_t rp0, int64_t rpE,
+                                         int lim_r, bool smem_rows, const int32_t* send, T* sprod, uint8_t* mark,
+                                         FV<T>* s_wagg, T* s_cin, int32_t* s_ffl) {
   constexpr int W = kSv3Threads / 32;
-  constexpr int ROWCAP = SLOTS + 256;          // row ends staged (more, i.e. empty rows: global reads)
-  __shared__ int32_t send[ROWCAP];             // local row ends E[r] of the owned rows
-  __shared__ __align__(16) T sprod[SLOTS + SLOTS / 8 + 4];   // products, then segmented sums
-  __shared__ __align__(16) uint8_t mark[SLOTS + 16];   // mark[q] = 1: a row starts at item q
-  __shared__ FV<T> s_wagg[W];
-  __shared__ T s_cin[kSv3Threads];             // sum flowing into thread t's leading run
-  __shared__ int32_t s_ffl[kSv3Threads];       // thread t's first flagged item (or its end)
-
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int p = blockIdx.x;
-  const int64_t s = ldg(a.ppos + p), e = ldg(a.ppos + p + 1);
-  const int64_t rp0 = ldg(a.prow + p), rpE = ldg(a.prow + p + 1);
-  const int n = (int)(e - s);                  // positions of this partition (<= SLOTS)
-  const int wb = w * WCH;                      // warp chunk [wb, wb + WCH) in local positions
-  // owned rows [0, lim_r) (R7): local ends E[r] = pos[rp0 + r + 1] - s, in [0, n]
-  const int lim_r = (int)((rpE < a.nouter ? rpE : a.nouter) - rp0);
-  const bool smem_rows = lim_r <= ROWCAP;
   const int64_t* __restrict__ gend = a.pos + rp0 + 1;
-
-  // 0. clear the row-start marks (V bytes per thread)
-  if constexpr (V == 16) reinterpret_cast<uint4*>(mark)[tid] = make_uint4(0, 0, 0, 0);
-  else if constexpr (V == 8) reinterpret_cast<uint2*>(mark)[tid] = make_uint2(0, 0);
-  else for (int i = 0; i < V; ++i) mark[tid * V + i] = 0;
-  // 1. products (crd / val read lane-strided: 128 contiguous bytes per warp instruction; the x
-  //    gathers of a long row touch a few lines instead of 32), staged row ends
-  if (n == SLOTS) sv3_products<T, V, true>(a, s, n, wb, lane, sprod);
-  else sv3_products<T, V, false>(a, s, n, wb, lane, sprod);
-  if (smem_rows)
-    for (int i = tid; i < lim_r; i += kSv3Threads) send[i] = (int32_t)(ldg(gend + i) - s);
-  __syncthreads();
   auto row_end = [&](int r) -> int32_t { return smem_rows ? send[r] : (int32_t)(ldg(gend + r) - s); };
   // 2. mark the row starts inside the tile: row r + 1 starts at E[r] (empty rows mark the same item)
   for (int r = tid; r < lim_r; r += kSv3Threads) {
@@ -195,6 +168,45 @@ __global__ void __launch_bounds__(kSv3Threads, Sv3Cfg<T>::MINB) spmv3_kernel(con
     a.carry_row[p] = has ? rpE : -1;
     a.carry_val[p] = (has && n > q0) ? seg_at(n - 1) : T(0);
   }
+}
+
+template <typename T, bool DY>
+__global__ void __launch_bounds__(kSv3Threads, Sv3Cfg<T>::MINB) spmv3_kernel(const __grid_constant__ SpmvArgs<T> a) {
+  constexpr int V = Sv3Cfg<T>::V;
+  constexpr int WCH = 32 * V;                  // positions per warp chunk
+  constexpr int SLOTS = kSv3Threads * V;
+  constexpr int W = kSv3Threads / 32;
+  constexpr int ROWCAP = SLOTS + 256;          // row ends staged (more, i.e. empty rows: global reads)
+  __shared__ int32_t send[ROWCAP];             // local row ends E[r] of the owned rows
+  __shared__ __align__(16) T sprod[SLOTS + SLOTS / 8 + 4];   // products, then segmented sums
+  __shared__ __align__(16) uint8_t mark[SLOTS + 16];   // mark[q] = 1: a row starts at item q
+  __shared__ FV<T> s_wagg[W];
+  __shared__ T s_cin[kSv3Threads];             // sum flowing into thread t's leading run
+  __shared__ int32_t s_ffl[kSv3Threads];       // thread t's first flagged item (or its end)
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int p = blockIdx.x;
+  const int64_t s = ldg(a.ppos + p), e = ldg(a.ppos + p + 1);
+  const int64_t rp0 = ldg(a.prow + p), rpE = ldg(a.prow + p + 1);
+  const int n = (int)(e - s);                  // positions of this partition (<= SLOTS)
+  const int wb = w * WCH;                      // warp chunk [wb, wb + WCH) in local positions
+  // owned rows [0, lim_r) (R7): local ends E[r] = pos[rp0 + r + 1] - s, in [0, n]
+  const int lim_r = (int)((rpE < a.nouter ? rpE : a.nouter) - rp0);
+  const bool smem_rows = lim_r <= ROWCAP;
+  const int64_t* __restrict__ gend = a.pos + rp0 + 1;
+
+  // 0. clear the row-start marks (V bytes per thread)
+  if constexpr (V == 16) reinterpret_cast<uint4*>(mark)[tid] = make_uint4(0, 0, 0, 0);
+  else if constexpr (V == 8) reinterpret_cast<uint2*>(mark)[tid] = make_uint2(0, 0);
+  else for (int i = 0; i < V; ++i) mark[tid * V + i] = 0;
+  // 1. products (crd / val read lane-strided: 128 contiguous bytes per warp instruction; the x
+  //    gathers of a long row touch a few lines instead of 32), staged row ends
+  if (n == SLOTS) sv3_products<T, V, true>(a, s, n, wb, lane, sprod);
+  else sv3_products<T, V, false>(a, s, n, wb, lane, sprod);
+  if (smem_rows)
+    for (int i = tid; i < lim_r; i += kSv3Threads) send[i] = (int32_t)(ldg(gend + i) - s);
+  __syncthreads();
+  sv3_tail<T, V, DY>(a, p, s, n, rp0, rpE, lim_r, smem_rows, send, sprod, mark, s_wagg, s_cin, s_ffl);
 }
 
 }  // namespace nacho
