@@ -262,6 +262,40 @@ __device__ __noinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t Q, 
   return b;
 }
 
+
+// First index of the run of `row` that ends at `end` in a carry-row array (the run is contiguous:
+// entries before it hold other rows or -1).  Warp-cooperative: exponential probes end - 2^lane
+// bracket the start, then 32-ary search -- O(log32 run) rounds of loads instead of a 32-per-round
+// walk (a dense row spans ~10^4..10^5 partitions).
+__device__ __forceinline__ int64_t warp_run_start(const int64_t* keys, int64_t end, int64_t row) {
+  const int lane = threadIdx.x & 31;
+  const int64_t probe = end - ((int64_t)1 << lane);
+  const bool in = probe >= 0 && lane < 62 && keys[probe < 0 ? 0 : probe] == row;
+  const unsigned m = __ballot_sync(kFull, in);
+  const int L = __ffs(~m) - 1;   // first lane whose probe left the run (m == kFull cannot happen below 2^31)
+  if (L < 0) return 0;
+  // the start lies in (end - 2^L, end - 2^(L-1)]  (L = 0: the start is end itself)
+  if (L == 0) return end;
+  int64_t hi = end - ((int64_t)1 << (L - 1));            // in the run
+  int64_t lo = end - ((int64_t)1 << L) + 1;              // first candidate
+  if (lo < 0) lo = 0;
+  // least j in [lo, hi] with keys[j] == row (a monotone predicate on this interval)
+  while (lo < hi) {
+    const int64_t span = hi - lo;
+    const int64_t x = lo + ((int64_t)lane * span) / 32;   // lane 0 probes lo
+    const bool ok = keys[x] == row;
+    const unsigned mm = __ballot_sync(kFull, ok);
+    const int f = __ffs(mm) - 1;                          // first lane inside the run
+    if (f < 0) { lo = __shfl_sync(kFull, x, 31) + 1; continue; }   // all probes before the start
+    const int64_t xf = __shfl_sync(kFull, x, f);
+    const int64_t xp = __shfl_sync(kFull, x, f > 0 ? f - 1 : 0);
+    if (f == 0) { hi = xf; break; }
+    lo = xp + 1;
+    hi = xf;
+  }
+  return hi;
+}
+
 // ------------------------------------------------------------------ scans
 template <typename T>
 __device__ __forceinline__ T warp_incl_sum(T v) {

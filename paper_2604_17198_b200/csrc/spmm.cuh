@@ -331,19 +331,18 @@ __global__ void spmm_fixup_kernel(SpmmArgs<T> a) {
     m &= m - 1;
     const int64_t row = __shfl_sync(kFull, key, l);
     const int64_t end = gw * 32 + l;
-    int64_t start = end;
-    for (;;) {
-      const int64_t j = start - 1 - lane;
-      const bool match = j >= 0 && a.carry_row[j] == row;
-      const unsigned mm = __ballot_sync(kFull, match);
-      if (mm == kFull) { start -= 32; continue; }
-      start -= __ffs(~mm) - 1;
-      break;
-    }
-    for (int c = lane; c < a.nb; c += 32) {
-      T sum = T(0);
-      for (int64_t j = start; j <= end; ++j) sum += a.carry_val[j * a.nb + c];
-      a.C[row * a.ldc + c] += sum;
+    const int64_t start = warp_run_start(a.carry_row, end, row);
+    for (int c = lane; c < a.nb; c += 32) {   // four independent partial sums per lane (ILP)
+      T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
+      int64_t j = start;
+      for (; j + 3 <= end; j += 4) {
+        s0 += a.carry_val[j * a.nb + c];
+        s1 += a.carry_val[(j + 1) * a.nb + c];
+        s2 += a.carry_val[(j + 2) * a.nb + c];
+        s3 += a.carry_val[(j + 3) * a.nb + c];
+      }
+      for (; j <= end; ++j) s0 += a.carry_val[j * a.nb + c];
+      a.C[row * a.ldc + c] += (s0 + s1) + (s2 + s3);
     }
   }
 }

@@ -161,15 +161,7 @@ __global__ void spmv_fixup_kernel(SpmvArgs<T> a) {
     m &= m - 1;
     const int64_t row = __shfl_sync(kFull, key, l);
     const int64_t end = gw * 32 + l;
-    int64_t start = end;
-    for (;;) {  // walk back to the run start
-      const int64_t j = start - 1 - lane;
-      const bool match = j >= 0 && a.carry_row[j] == row;
-      const unsigned mm = __ballot_sync(kFull, match);
-      if (mm == kFull) { start -= 32; continue; }
-      start -= __ffs(~mm) - 1;
-      break;
-    }
+    const int64_t start = warp_run_start(a.carry_row, end, row);
     T sum = T(0);
     for (int64_t j = start + lane; j <= end; j += 32) sum += a.carry_val[j];
 #pragma unroll
