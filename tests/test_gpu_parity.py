@@ -214,6 +214,28 @@ def test_spadd_edge_cases():
                           for A in ops], P)
 
 
+def test_spadd_wide_keys():
+    """Hypersparse operands whose partitions span more rows than 32-bit (row, column) keys can hold
+    next to a wide column range: the 64-bit key path (index-only merge buffers) of spadd4."""
+    rng = np.random.default_rng(77)
+    M, Nc = 3_000_000, 2_000_000
+    ops = []
+    base_rows = np.sort(rng.choice(M, size=4000, replace=False))
+    for o in range(3):
+        keep = base_rows[rng.random(len(base_rows)) < 0.7]
+        extra = np.sort(rng.choice(M, size=1500, replace=False))
+        rows = np.concatenate([np.repeat(keep, 2), extra])
+        cols = np.concatenate([np.stack([rng.integers(0, Nc // 2, len(keep)),
+                                         rng.integers(Nc // 2, Nc, len(keep))], 1).ravel(),
+                               rng.integers(0, Nc, len(extra))])
+        key = np.unique(rows.astype(np.int64) * Nc + cols)
+        r, c = key // Nc, key % Nc
+        vals = rng.integers(-4, 5, len(r)).astype(np.float32)
+        ops.append(W.from_coo(r, c, vals, M, Nc))
+    for P in (None, 3, 40):
+        _spadd_check(ops, P)
+
+
 @pytest.mark.parametrize("values", ["int", "uniform"])
 def test_spadd_c2_scaled(values):
     wl = W.build("c2", 0.05, values=values, kmax=8)
