@@ -195,23 +195,24 @@ __device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&
 #pragma unroll
   for (int o = 0; o < KM; ++o)
     if (o < k) e[o] = (lane < hi[o] - lo[o]) ? (int32_t)ldg(a.op[o].crd + lo[o] + lane) : INF;
+  // rank of lane l's entry of window o in the multiset union ordered by (column, operand):
+  // entries of lower operands with a column <= it, of higher operands with a column < it, and the l
+  // entries before it in its own window -- unique ranks, so exactly one entry has rank R
   int32_t vstar = INF;
-  bool found = false;
 #pragma unroll
   for (int o = 0; o < KM; ++o) {
     if (o < k) {
-      int64_t less = 0, leq = 0;
+      const int32_t x = e[o];
+      int64_t rank = lane;
 #pragma unroll
       for (int o2 = 0; o2 < KM; ++o2) {
-        if (o2 < k) {
+        if (o2 < k && o2 != o) {
           const int n2 = (int)(hi[o2] - lo[o2]);
-          less += lanes_less(e[o2], e[o], n2);
-          leq += lanes_less(e[o2], e[o] == INF ? INF : e[o] + 1, n2);
+          rank += lanes_less(e[o2], (o2 < o && x != INF) ? x + 1 : x, n2);
         }
       }
-      const bool hit = e[o] != INF && less <= R && R < leq;
-      const unsigned hm = __ballot_sync(kFull, hit);
-      if (hm && !found) { vstar = __shfl_sync(kFull, e[o], __ffs(hm) - 1); found = true; }
+      const unsigned hm = __ballot_sync(kFull, x != INF && rank == R);
+      if (hm) vstar = __shfl_sync(kFull, x, __ffs(hm) - 1);
     }
   }
   b.col = vstar;
