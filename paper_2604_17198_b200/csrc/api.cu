@@ -213,7 +213,7 @@ nacho_status launch_spadd(const SpaddArgs<T>& a, cudaStream_t st) {
 template <typename T, int MODE, int KM>
 nacho_status launch_spadd4_k(const Spadd4Args<T>& a, cudaStream_t st) {
   auto kern = spadd4_kernel<T, MODE, KM>;
-  const size_t smem = sizeof(S4Shared<T>);
+  const size_t smem = sizeof(S4Shared<T, s4_small(MODE, KM)>);
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

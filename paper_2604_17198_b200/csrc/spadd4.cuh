@@ -57,7 +57,6 @@ constexpr int kS4Vt = NACHO_S4_VT;                // merged entries per thread a
 constexpr int kS4Tile = kS4Threads * kS4Vt;       // entries per partition
 constexpr int kS4Buf = kS4Tile + kS4Tile / 16 + 8;   // padded stage-buffer capacity (elements)
 constexpr int kS4PosRound = 8;                    // row pointers loaded per thread and round
-constexpr int kS4PosCap = 2 * kS4Threads * kS4PosRound;   // staged row pointers (all operands)
 
 template <typename T>
 struct Spadd4Args {
@@ -76,8 +75,10 @@ struct Spadd4Args {
 template <typename KT>
 __device__ __forceinline__ int s4pd(int i) { return sizeof(KT) == 4 ? i + (i >> 5) : i + (i >> 4); }
 
-// Shared memory (one static block; the 64-bit operand keys alias the 32-bit stage key buffers).
-template <typename T>
+// Shared memory.  SMALL (fill / stage modes with k <= 3): one stage buffer and no union buffers, so
+// five CTAs fit an SM; the 64-bit operand keys then span zk + uv (uv must follow zk).  Otherwise two
+// stage key buffers (the 64-bit keys alias them) and three source buffers.
+template <typename T, bool SMALL = false>
 struct S4Shared {
   int64_t b0pos[NACHO_MAX_K];
   int32_t off[NACHO_MAX_K + 1];           // concatenation offsets; off[o] = INT32_MAX for o > k
@@ -91,10 +92,15 @@ struct S4Shared {
   int32_t cmn[kS4Threads / 32], cmx[kS4Threads / 32];
   alignas(16) T val[kS4Tile];                     // operand values (concatenated)
   alignas(16) int32_t col[kS4Buf];                // columns (padded slots); 32-bit path: the keys in place
-  alignas(16) uint32_t zk[2 * kS4Buf];            // 32-bit path: stage keys | 64-bit path: operand keys
-  alignas(16) uint16_t zs[3 * kS4Buf];            // stage sources (2) + union sources
+  alignas(16) uint32_t zk[(SMALL ? 1 : 2) * kS4Buf];   // 32-bit path: stage keys | 64-bit: operand keys
   alignas(16) T uv[kS4Buf];                       // union values; before that: the row marks
+  alignas(16) uint16_t zs[(SMALL ? 1 : 3) * kS4Buf];   // stage sources (+ union sources)
+  static constexpr int kPosCap = SMALL ? kS4Threads * kS4PosRound : 2 * kS4Threads * kS4PosRound;
 };
+static_assert(sizeof(uint32_t) * kS4Buf % 16 == 0, "uv must start right after zk");
+
+// The SMALL layout serves the emitting modes with at most three operands.
+__host__ __device__ constexpr bool s4_small(int mode, int km) { return (mode == kS4Fill || mode == kS4Stage) && km <= 3; }
 
 // "Last mark wins" combine for the row scan: (f, v) . (f2, v2) = (f | f2, f2 ? v2 : v).
 __device__ __forceinline__ void s4_mark_op(int& f, int& v, int f2, int v2) {
@@ -406,8 +412,8 @@ __device__ __forceinline__ int64_t s4_lookback(unsigned long long* st, int64_t p
 
 // Union of the keyed operands (K: concatenated operand keys).  KIND of the stage buffers: 1 (keyed,
 // 32-bit) or 2 (index-only, 64-bit).  Returns nu; US / UV hold the union.
-template <typename T, typename KT, bool VALS, int KIND>
-__device__ __forceinline__ int s4_union(S4Shared<T>& sh, int k, const KT* K, KT* Z1, KT* Z2, uint16_t* S1,
+template <typename T, typename KT, bool VALS, int KIND, class SH>
+__device__ __forceinline__ int s4_union(SH& sh, int k, const KT* K, KT* Z1, KT* Z2, uint16_t* S1,
                                         uint16_t* S2, uint16_t* US, T* UV) {
   const int* off = sh.off;
   if (k == 1) {
@@ -440,8 +446,8 @@ __device__ __forceinline__ int s4_union(S4Shared<T>& sh, int k, const KT* K, KT*
 }
 
 // s4_union with a directly emitting final stage.
-template <typename T, typename KT, int KIND>
-__device__ __forceinline__ int s4_union_emit(S4Shared<T>& sh, int k, const KT* K, KT* Z1, KT* Z2, uint16_t* S1,
+template <typename T, typename KT, int KIND, class SH>
+__device__ __forceinline__ int s4_union_emit(SH& sh, int k, const KT* K, KT* Z1, KT* Z2, uint16_t* S1,
                                              uint16_t* S2, const S4Out<T>& out) {
   const int* off = sh.off;
   if (k <= 2) {
@@ -471,8 +477,8 @@ __device__ __forceinline__ int s4_union_emit(S4Shared<T>& sh, int k, const KT* K
 }
 
 // Keys (32- or 64-bit), union, offset and writes of one partition.
-template <typename T, typename KT, int MODE, int KM>
-__device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh, int64_t p, int n, int64_t row0,
+template <typename T, typename KT, int MODE, int KM, class SH>
+__device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, SH& sh, int64_t p, int n, int64_t row0,
                                         int64_t row1, int cb, int32_t cmin, unsigned long long& s4t) {
   (void)s4t;
   constexpr bool VALS = MODE != kS4Count;
@@ -546,12 +552,12 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh,
       out.pos_off = 0;
     }
     if (p == 0 && tid == 0) a.z_pos[0] = 0;
-    const int nu = s4_union_emit<T, KT, KIND>(sh, k, K, Z1, Z2, S1, S2, out);
+    const int nu = s4_union_emit<T, KT, KIND, SH>(sh, k, K, Z1, Z2, S1, S2, out);
     if (MODE == kS4Stage && tid == 0) a.part_cnt[p] = nu;
     S4PH(4);
     return;
   }
-  const int nu = s4_union<T, KT, VALS, KIND>(sh, k, K, Z1, Z2, S1, S2, US, sh.uv);
+  const int nu = s4_union<T, KT, VALS, KIND, SH>(sh, k, K, Z1, Z2, S1, S2, US, sh.uv);
   S4PH(4);
   if (MODE == kS4Count) {
     if (tid == 0) a.part_cnt[p] = nu;
@@ -603,10 +609,11 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, S4Shared<T>& sh,
 
 // KM: compile-time operand count (1..4), or NACHO_MAX_K for any k (read from a.ops.k).
 template <typename T, int MODE, int KM>
-__global__ void __launch_bounds__(kS4Threads, NACHO_S4_MINB) spadd4_kernel(const __grid_constant__ Spadd4Args<T> a) {
+__global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 5 : NACHO_S4_MINB) spadd4_kernel(const __grid_constant__ Spadd4Args<T> a) {
   constexpr bool VALS = MODE != kS4Count;
   extern __shared__ __align__(16) unsigned char s4raw[];
-  S4Shared<T>& sh = *reinterpret_cast<S4Shared<T>*>(s4raw);
+  using SH = S4Shared<T, s4_small(MODE, KM)>;
+  SH& sh = *reinterpret_cast<SH*>(s4raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int k = KM < NACHO_MAX_K ? KM : a.ops.k;
   int64_t p;
@@ -657,7 +664,7 @@ __global__ void __launch_bounds__(kS4Threads, NACHO_S4_MINB) spadd4_kernel(const
   int32_t* mark = reinterpret_cast<int32_t*>(sh.uv);
   int32_t* spos = reinterpret_cast<int32_t*>(sh.zk);   // [k][span + 1], free until the merges
   const int np = (int)span + 1;
-  const bool pre = span > 0 && (int64_t)k * np <= kS4PosCap;
+  const bool pre = span > 0 && (int64_t)k * np <= SH::kPosCap;
   int32_t cmn = INT32_MAX, cmx = -1;
   {
     int32_t c[kS4Vt];
@@ -680,7 +687,7 @@ __global__ void __launch_bounds__(kS4Threads, NACHO_S4_MINB) spadd4_kernel(const
     if (pre) {
       // flattened (operand, pointer) index f = tid + 256 m -> (po, pi) = (f / np, f % np)
 #pragma unroll
-      for (int half = 0; half < kS4PosCap / (kS4Threads * kS4PosRound); ++half) {
+      for (int half = 0; half < SH::kPosCap / (kS4Threads * kS4PosRound); ++half) {
         int64_t pv[kS4PosRound];
 #pragma unroll
         for (int m = 0; m < kS4PosRound; ++m) {
@@ -744,8 +751,8 @@ __global__ void __launch_bounds__(kS4Threads, NACHO_S4_MINB) spadd4_kernel(const
   S4PH(2);
   const int cb = 32 - __clz((unsigned)(cmax - cmin));                       // column bits (0 if one column)
   const int rb = span > 0 ? 64 - __clzll((unsigned long long)span) : 0;      // local row bits
-  if (rb + cb <= 31) s4_body<T, uint32_t, MODE, KM>(a, sh, p, n, row0, row1, cb, cmin, s4t);
-  else s4_body<T, uint64_t, MODE, KM>(a, sh, p, n, row0, row1, 32, cmin, s4t);
+  if (rb + cb <= 31) s4_body<T, uint32_t, MODE, KM, SH>(a, sh, p, n, row0, row1, cb, cmin, s4t);
+  else s4_body<T, uint64_t, MODE, KM, SH>(a, sh, p, n, row0, row1, 32, cmin, s4t);
 }
 
 // Places the staged unions (kS4Stage): partition p's union moves from its provisional offset
