@@ -767,9 +767,20 @@ __global__ void __launch_bounds__(kS4Threads) s4_compact_kernel(const __grid_con
   int64_t prov = 0;
   for (int o = 0; o < k; ++o) prov += ldg(a.parts.pos + p * k + o);
   const int64_t off = ldg(a.part_off + p), nu = ldg(a.part_off + p + 1) - off;
-  for (int64_t j = threadIdx.x; j < nu; j += kS4Threads) {
-    a.z_crd[off + j] = t_crd[prov + j];
-    a.z_val[off + j] = t_val[prov + j];
+  constexpr int U = 4;   // loads in flight per thread
+  for (int64_t jb = 0; jb < nu; jb += U * kS4Threads) {
+    int32_t c[U];
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = jb + u * kS4Threads + threadIdx.x;
+      if (j < nu) { c[u] = __ldcs(t_crd + prov + j); v[u] = __ldcs(t_val + prov + j); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = jb + u * kS4Threads + threadIdx.x;
+      if (j < nu) { a.z_crd[off + j] = c[u]; a.z_val[off + j] = v[u]; }
+    }
   }
   const int64_t r0 = ldg(a.parts.row + p), r1 = ldg(a.parts.row + p + 1);
   for (int64_t r = r0 + threadIdx.x; r < r1; r += kS4Threads) a.z_pos[r + 1] += off;
