@@ -131,7 +131,7 @@ __device__ __forceinline__ int lanes_less(V v, V x, int n) {
 // KM: compile-time bound on k (register arrays sized KM).  Column values are int32 (crd < ncols <=
 // INT32_MAX), so INT32_MAX is a safe "past the window" value.
 template <int KM>
-__device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&lo)[KM], int64_t (&hi)[KM], int64_t R,
+__device__ __forceinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&lo)[KM], int64_t (&hi)[KM], int64_t R,
                                               Boundary& b) {
   const int lane = threadIdx.x & 31;
   constexpr int32_t INF = INT32_MAX;
@@ -229,7 +229,7 @@ __device__ __noinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&
 // over column values in which every lane runs the per-operand lb_search of Listing 7 inside windows
 // that narrow round by round.
 template <int KM = NACHO_MAX_K>
-__device__ __noinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t Q, int64_t outer_lo, int64_t outer_hi) {
+__device__ __forceinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t Q, int64_t outer_lo, int64_t outer_hi) {
   Boundary b;
   const int k = a.k;
   // ---- level i
