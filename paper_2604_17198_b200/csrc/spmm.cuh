@@ -332,6 +332,32 @@ __global__ void spmm_fixup_kernel(SpmmArgs<T> a) {
     const int64_t row = __shfl_sync(kFull, key, l);
     const int64_t end = gw * 32 + l;
     const int64_t start = warp_run_start(a.carry_row, end, row);
+    if (end - start >= 64) {
+      // long run (a dense row's carries): lanes stride over the partitions, each summing 8 columns at
+      // a time, then a shuffle tree per column -- a fixed order, so deterministic for a given P
+      for (int c0 = 0; c0 < a.nb; c0 += 8) {
+        T acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = T(0);
+        for (int64_t j = start + lane; j <= end; j += 32) {
+          const T* cv = a.carry_val + j * a.nb + c0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) if (c0 + u < a.nb) acc[u] += cv[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) acc[u] += __shfl_xor_sync(kFull, acc[u], d);
+        }
+        if (lane < 8 && c0 + lane < a.nb) {
+          T v = acc[0];
+#pragma unroll
+          for (int u = 1; u < 8; ++u) v = lane == u ? acc[u] : v;
+          a.C[row * a.ldc + c0 + lane] += v;
+        }
+      }
+      continue;
+    }
     for (int c = lane; c < a.nb; c += 32) {   // four independent partial sums per lane (ILP)
       T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
       int64_t j = start;

@@ -32,6 +32,8 @@ def main():
         f(buf, 1)
         if mode == "fused":
             N.spadd_k_fused(ops, parts, zp, zc, zv, part_off=off)
+        elif mode == "staged":
+            N.spadd_k_staged(ops, parts, zp, zc, zv, part_off=off)
         else:
             N.spadd_k_count(ops, parts, off)
         torch.cuda.synchronize()
