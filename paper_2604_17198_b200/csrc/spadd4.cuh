@@ -56,6 +56,7 @@ constexpr int kS4Threads = 256;
 constexpr int kS4Vt = NACHO_S4_VT;                // merged entries per thread and stage
 constexpr int kS4Tile = kS4Threads * kS4Vt;       // entries per partition
 constexpr int kS4Buf = kS4Tile + kS4Tile / 16 + 8;   // padded stage-buffer capacity (elements)
+constexpr int kS4DenseWords = 2048;               // widest column range of the bitmap path (x 32 columns)
 constexpr int kS4PosRound = 8;                    // row pointers loaded per thread and round
 
 template <typename T>
@@ -476,6 +477,138 @@ __device__ __forceinline__ int s4_union_emit(SH& sh, int k, const KT* K, KT* Z1,
                                    out);
 }
 
+// Single-row partitions with a narrow column range (the bulk of a power-law matrix's heavy rows):
+// the union is a bitmap.  Each operand's columns set bits of its bitmap, the union bitmap's prefix
+// popcounts give every column its union index, values fold into that slot operand by operand (left
+// fold in operand order, R9), and the set bits of the union bitmap are the output columns.  No keys,
+// no merge-path stages: a handful of instructions per entry.
+template <typename T, int MODE, int KM, class SH>
+__device__ __forceinline__ void s4_dense(const Spadd4Args<T>& a, SH& sh, int64_t p, int n, int64_t row0,
+                                         int64_t row1, int32_t cmin, int nw) {
+  constexpr bool VALS = MODE != kS4Count;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int k = KM < NACHO_MAX_K ? KM : a.ops.k;
+  uint32_t* bm = sh.zk;                 // [k][nw] operand bitmaps
+  uint32_t* U = bm + k * nw;            // [nw] union bitmap
+  int32_t* pre = reinterpret_cast<int32_t*>(U + nw);   // [nw] union entries before word w
+  T* ov = sh.uv;                        // [nu] folded union values
+  for (int i = tid; i < (k + 1) * nw; i += kS4Threads) bm[i] = 0u;
+  __syncthreads();
+  int ob[KM > 1 ? KM - 1 : 1];
+#pragma unroll
+  for (int o = 0; o < KM - 1; ++o) ob[o] = sh.off[o + 1];
+  for (int j = tid; j < n; j += kS4Threads) {
+    int o = 0;
+#pragma unroll
+    for (int oo = 0; oo < KM - 1; ++oo) o += j >= ob[oo] ? 1 : 0;
+    const int c = sh.col[s4pd<uint32_t>(j)] - cmin;
+    atomicOr(&bm[o * nw + (c >> 5)], 1u << (c & 31));
+  }
+  __syncthreads();
+  // union bitmap and its exclusive prefix popcount (block scan over the words)
+  constexpr int WPT = 4;                // words per thread and round
+  int carry = 0;
+  for (int w0 = 0; w0 < nw; w0 += kS4Threads * WPT) {
+    uint32_t u[WPT];
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const int ww = w0 + tid * WPT + q;
+      u[q] = 0u;
+      if (ww < nw) {
+#pragma unroll
+        for (int o = 0; o < KM; ++o) if (o < k) u[q] |= bm[o * nw + ww];
+        U[ww] = u[q];
+      }
+      c += __popc(u[q]);
+    }
+    int inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += v;
+    }
+    if (lane == 31) sh.ired[w] = inc;
+    __syncthreads();
+    int before = carry, tot = 0;
+#pragma unroll
+    for (int ww = 0; ww < kS4Threads / 32; ++ww) {
+      const int v = sh.ired[ww];
+      before += ww < w ? v : 0;
+      tot += v;
+    }
+    int x = before + inc - c;
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const int ww = w0 + tid * WPT + q;
+      if (ww < nw) pre[ww] = x;
+      x += __popc(u[q]);
+    }
+    carry += tot;
+    __syncthreads();
+  }
+  const int nu = carry;
+  // values: operand by operand, each entry into its union slot (= if no lower operand has the column)
+  if (VALS) {
+    for (int o = 0; o < k; ++o) {
+      for (int j = sh.off[o] + tid; j < sh.off[o + 1]; j += kS4Threads) {
+        const int c = sh.col[s4pd<uint32_t>(j)] - cmin;
+        const int ww = c >> 5;
+        const uint32_t bit = 1u << (c & 31);
+        const int r = pre[ww] + __popc(U[ww] & (bit - 1u));
+        bool prior = false;
+#pragma unroll
+        for (int o2 = 0; o2 < KM; ++o2) if (o2 < o) prior = prior || (bm[o2 * nw + ww] & bit) != 0u;
+        const T v = sh.val[j];
+        ov[r] = prior ? ov[r] + v : v;
+      }
+      __syncthreads();
+    }
+  }
+  if (MODE == kS4Count) {
+    if (tid == 0) a.part_cnt[p] = nu;
+    return;
+  }
+  int64_t off, pos_off;
+  if (MODE == kS4Fill) {
+    off = ldg(a.part_off + p);
+    pos_off = off;
+  } else if (MODE == kS4Stage) {
+    off = 0;
+#pragma unroll
+    for (int o = 0; o < KM; ++o) if (o < k) off += sh.b0pos[o];
+    pos_off = 0;
+    if (tid == 0) a.part_cnt[p] = nu;
+  } else {
+    if (w == 0) {
+      const int64_t ex = s4_lookback(a.lb_state, p, nu);
+      if (lane == 0) {
+        sh.bcast = ex;
+        if (a.part_off) { a.part_off[p] = ex; if (p == a.parts.P - 1) a.part_off[a.parts.P] = ex + nu; }
+      }
+    }
+    __syncthreads();
+    off = sh.bcast;
+    pos_off = off;
+  }
+  if (p == 0 && tid == 0) a.z_pos[0] = 0;
+  // output: the set bits of the union bitmap, word by word
+  for (int ww = tid; ww < nw; ww += kS4Threads) {
+    uint32_t bits = U[ww];
+    int idx = pre[ww];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      a.z_crd[off + idx] = cmin + 32 * ww + b;
+      a.z_val[off + idx] = ov[idx];
+      ++idx;
+    }
+  }
+  // the partition's one row completes here iff b_{p+1} lies in a later row (R7); trailing empty rows
+  // of the last partition follow it
+  for (int64_t r = tid; r < row1 - row0; r += kS4Threads) a.z_pos[row0 + r + 1] = pos_off + nu;
+}
+
 // Keys (32- or 64-bit), union, offset and writes of one partition.
 template <typename T, typename KT, int MODE, int KM, class SH>
 __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, SH& sh, int64_t p, int n, int64_t row0,
@@ -724,6 +857,22 @@ __global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 5 : NACHO_S4_
   if (lane == 0) { sh.cmn[w] = cmn; sh.cmx[w] = cmx; }
   __syncthreads();
   S4PH(1);
+  int32_t cmin = INT32_MAX, cmax = -1;
+#pragma unroll
+  for (int ww = 0; ww < kS4Threads / 32; ++ww) { cmin = min(cmin, sh.cmn[ww]); cmax = max(cmax, sh.cmx[ww]); }
+  if (cmax < cmin) { cmin = 0; cmax = 0; }
+  // ---- one row, narrow column range: bitmap union (s4_dense)
+  {
+    const int nw = (int)(((int64_t)cmax - cmin) / 32 + 1);
+    if (span == 0 && (int64_t)nw * (k + 2) <= (int64_t)(sizeof(sh.zk) / 4) && nw <= kS4DenseWords) {
+      s4_dense<T, MODE, KM, SH>(a, sh, p, n, row0, row1, cmin, nw);
+      S4PH(5);   // phase-timer slot 5: bitmap partitions
+#ifdef NACHO_PROF
+      if (tid == 0 && (p & 15) == 0) atomicAdd(&g_phase[7], 1ull);
+#endif
+      return;
+    }
+  }
   // ---- rows (row0, row0 + span] starting inside operand o's range mark their first entry (non-empty)
   for (int o = 0; o < k; ++o) {
     const int base = sh.off[o], no = sh.off[o + 1] - base;
@@ -743,10 +892,6 @@ __global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 5 : NACHO_S4_
       }
     }
   }
-  int32_t cmin = INT32_MAX, cmax = -1;
-#pragma unroll
-  for (int ww = 0; ww < kS4Threads / 32; ++ww) { cmin = min(cmin, sh.cmn[ww]); cmax = max(cmax, sh.cmx[ww]); }
-  if (cmax < cmin) { cmin = 0; cmax = 0; }
   __syncthreads();
   S4PH(2);
   const int cb = 32 - __clz((unsigned)(cmax - cmin));                       // column bits (0 if one column)

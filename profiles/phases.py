@@ -11,7 +11,7 @@ import torch  # noqa: E402
 import paper_2604_17198_b200 as N  # noqa: E402
 import workloads as W  # noqa: E402
 
-NAMES = ["ticket+bounds", "loads", "marks", "keys", "union", "offset", "writes", "-"]
+NAMES = ["ticket+bounds", "loads", "marks", "keys", "union", "bitmap path / offset", "writes", "#bitmap (count)"]
 
 
 def main():
