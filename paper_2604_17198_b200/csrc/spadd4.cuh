@@ -741,6 +741,14 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, SH& sh, int64_t 
 }
 
 // KM: compile-time operand count (1..4), or NACHO_MAX_K for any k (read from a.ops.k).
+// The 64-bit key path is rare (very wide partitions); kept out of line so it does not crowd the
+// instruction cache of the hot 32-bit and bitmap paths.
+template <typename T, int MODE, int KM, class SH>
+__device__ __noinline__ void s4_body64(const Spadd4Args<T>& a, SH& sh, int64_t p, int n, int64_t row0, int64_t row1,
+                                       int32_t cmin, unsigned long long& s4t) {
+  s4_body<T, uint64_t, MODE, KM, SH>(a, sh, p, n, row0, row1, 32, cmin, s4t);
+}
+
 template <typename T, int MODE, int KM>
 __global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 5 : NACHO_S4_MINB) spadd4_kernel(const __grid_constant__ Spadd4Args<T> a) {
   constexpr bool VALS = MODE != kS4Count;
@@ -897,7 +905,7 @@ __global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 5 : NACHO_S4_
   const int cb = 32 - __clz((unsigned)(cmax - cmin));                       // column bits (0 if one column)
   const int rb = span > 0 ? 64 - __clzll((unsigned long long)span) : 0;      // local row bits
   if (rb + cb <= 31) s4_body<T, uint32_t, MODE, KM, SH>(a, sh, p, n, row0, row1, cb, cmin, s4t);
-  else s4_body<T, uint64_t, MODE, KM, SH>(a, sh, p, n, row0, row1, 32, cmin, s4t);
+  else s4_body64<T, MODE, KM, SH>(a, sh, p, n, row0, row1, cmin, s4t);
 }
 
 // Places the staged unions (kS4Stage): partition p's union moves from its provisional offset
