@@ -46,7 +46,10 @@ __device__ unsigned long long g_phase[16];
 #define S4PH_INIT unsigned long long s4t = 0
 #endif
 
-constexpr int kS4Threads = 256;
+#ifndef NACHO_S4_THREADS   // tuning override
+#define NACHO_S4_THREADS 256
+#endif
+constexpr int kS4Threads = NACHO_S4_THREADS;
 #ifndef NACHO_S4_VT   // tuning override
 #define NACHO_S4_VT 8
 #endif
@@ -750,7 +753,7 @@ __device__ __noinline__ void s4_body64(const Spadd4Args<T>& a, SH& sh, int64_t p
 }
 
 template <typename T, int MODE, int KM>
-__global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 5 : NACHO_S4_MINB) spadd4_kernel(const __grid_constant__ Spadd4Args<T> a) {
+__global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 1280 / kS4Threads : NACHO_S4_MINB) spadd4_kernel(const __grid_constant__ Spadd4Args<T> a) {
   constexpr bool VALS = MODE != kS4Count;
   extern __shared__ __align__(16) unsigned char s4raw[];
   using SH = S4Shared<T, s4_small(MODE, KM)>;
