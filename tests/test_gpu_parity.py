@@ -214,6 +214,18 @@ def test_spadd_edge_cases():
                           for A in ops], P)
 
 
+def test_spadd_fp64():
+    """fp64 values through every SpAdd path (count / fill, fused, staged; bitmap and merge-path
+    partitions): bit-exact left folds against the oracle."""
+    rng = np.random.default_rng(91)
+    for k in (2, 3, 5):
+        ops32 = _random_ops(rng, k, 700, 3000, 0.004, dense_rows=[11, 500])
+        ops = [W.SparseMatrix(A.format, A.nrows, A.ncols, A.pos, A.crd,
+                              rng.uniform(-2, 2, A.nnz).astype(np.float64)) for A in ops32]
+        for P in (None, 4, 97):
+            _spadd_check(ops, P)
+
+
 def test_spadd_wide_keys():
     """Hypersparse operands whose partitions span more rows than 32-bit (row, column) keys can hold
     next to a wide column range: the 64-bit key path (index-only merge buffers) of spadd4."""
