@@ -164,14 +164,14 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
             N.partition(ops, P, out=parts)
             if timed:
                 m.append(ev(torch))
-            dist.spadd(ops, parts)          # local single-pass SpAdd + NCCL all-gather of the Z segments
+            dist.spadd(ops, parts)          # local staged single-read SpAdd + NCCL all-gather of the Z segments
             if timed:
                 m.append(ev(torch))
             return m
-        times, sec = timer.run(step_dist, args.steps, args.warmup, ["partition", "spadd_fused+exchange"], soak_s=1.0)
+        times, sec = timer.run(step_dist, args.steps, args.warmup, ["partition", "spadd_staged+exchange"], soak_s=1.0)
         vs = ops[0].val.element_size()
         return dict(work=qstar, times=times, sec=sec, launches=5, algo_step=0, nnz_z=0, P=P,
-                    kernel_bytes={"spadd_fused+exchange": sum(n * (4 + vs) for n in nnz), "partition": 1},
+                    kernel_bytes={"spadd_staged+exchange": sum(n * (4 + vs) for n in nnz), "partition": 1},
                     two_pass={}, dtype="f32" if vs == 4 else "f64", wl=wl, parts=parts)
     part_off = torch.empty(local.P + 1, dtype=torch.int64, device="cuda")
     arr = N._matrices(ops)

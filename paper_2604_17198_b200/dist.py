@@ -181,13 +181,13 @@ def spadd_assemble(nrows: int, z_pos_local: torch.Tensor, z_crd_local: torch.Ten
 
 
 def spadd(ops, parts, group=None):
-    """Distributed k-way SpAdd on the CUDA kernels (single-pass kernel on each rank's slice)."""
-    from . import spadd_k_fused
+    """Distributed k-way SpAdd on the CUDA kernels (single-read staged path on each rank's slice)."""
+    from . import spadd_k_staged
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     lo, hi = rank_range(parts.P, world, rank)
     view = slice_parts(parts, lo, hi)
     part_off = torch.empty(view.P + 1, dtype=torch.int64, device=ops[0].pos.device)
-    z_pos, z_crd, z_val = spadd_k_fused(ops, view, part_off=part_off)
+    z_pos, z_crd, z_val = spadd_k_staged(ops, view, part_off=part_off)
     nnz_local = int(part_off[-1].item())
     own_lo = int(parts.row[lo].item())
     own_hi = int(parts.row[hi].item())

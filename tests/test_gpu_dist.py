@@ -37,7 +37,8 @@ def test_spmv_device_slices(ndev):
 
 
 @pytest.mark.parametrize("ndev", [2, 8])
-def test_spadd_device_slices(ndev):
+@pytest.mark.parametrize("path", ["fused", "staged"])
+def test_spadd_device_slices(ndev, path):
     wl = W.build("c2", 0.02, device="cuda", values="int", kmax=8)
     ops = wl.ops
     P = ndev * ((N.auto_partitions(ops, "spadd") + ndev - 1) // ndev)
@@ -47,7 +48,8 @@ def test_spadd_device_slices(ndev):
         lo, hi = D.rank_range(P, ndev, d)
         view = D.slice_parts(parts, lo, hi)
         off = torch.empty(view.P + 1, dtype=torch.int64, device="cuda")
-        zp, zc, zv = N.spadd_k_fused(ops, view, part_off=off)
+        run = N.spadd_k_staged if path == "staged" else N.spadd_k_fused
+        zp, zc, zv = run(ops, view, part_off=off)
         pieces.append((zp, zc, zv, int(off[-1].item()), int(parts.row[lo].item()), int(parts.row[hi].item())))
     zp, zc, zv = D.spadd_combine(pieces, ops[0].nrows, "cuda")
     rp, rc, rv = O.spadd_k([A.numpy() for A in ops])
