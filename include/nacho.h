@@ -85,6 +85,14 @@ typedef struct {
  * Errors: INVALID_ARG (k, P, nulls, DCSR with k > 1), SHAPE (mismatched operands), OVERFLOW. */
 nacho_status nacho_partition(const nacho_matrix* ops, int32_t k, int32_t P, nacho_parts* out, void* stream);
 
+/* nacho_partition_slice -- the boundaries p_begin .. p_begin + out->P of the P-partition (the same
+ * values nacho_partition writes at those indices), into out[0 .. out->P]: a device's share of a
+ * device-level cut (device d runs partitions [d P_l, (d+1) P_l) of P = D P_l), so each
+ * device searches only its own P_l + 1 boundaries.  The queries stay Q_p = floor(p Q* / P).
+ * Errors: as nacho_partition; INVALID_ARG when [p_begin, p_begin + out->P] leaves [0, P]. */
+nacho_status nacho_partition_slice(const nacho_matrix* ops, int32_t k, int32_t P, int32_t p_begin, nacho_parts* out,
+                                   void* stream);
+
 /* Partition count the kernels below pick when the caller does not fix P: ceil(Q* / tile), tile being
  * the per-CTA work of the kernel for that operation (op: 0 spmv, 1 spadd, 2 spmm). */
 int32_t nacho_auto_partitions(const nacho_matrix* ops, int32_t k, int32_t op);

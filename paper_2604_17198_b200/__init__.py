@@ -48,6 +48,7 @@ def _load():
     L = ctypes.CDLL(LIB_PATH)
     vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
     L.nacho_partition.argtypes = [vp, i32, i32, vp, vp]
+    L.nacho_partition_slice.argtypes = [vp, i32, i32, i32, vp, vp]
     L.nacho_auto_partitions.argtypes = [vp, i32, i32]
     L.nacho_auto_partitions.restype = i32
     L.nacho_spmv_workspace_size.argtypes = [vp, i32]
@@ -73,7 +74,7 @@ def _load():
 
 lib = _load()
 
-EXPORTS = ["nacho_partition", "nacho_auto_partitions", "nacho_spmv_workspace_size", "nacho_spmv",
+EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", "nacho_spmv_workspace_size", "nacho_spmv",
            "nacho_spadd_k_workspace_size", "nacho_spadd_k_count", "nacho_spadd_k_fill", "nacho_spadd_k",
            "nacho_spadd_k_staged_workspace_size", "nacho_spadd_k_staged",
            "nacho_spmm_workspace_size", "nacho_spmm", "nacho_validate", "nacho_last_error",
@@ -167,6 +168,15 @@ def partition(ops, P: int, out: Parts = None, stream=None) -> Parts:
     out = out or Parts(P, len(ops), ops[0].pos.device)
     pc = out.c()
     _check(lib.nacho_partition(arr, len(ops), P, ctypes.byref(pc), _stream(stream)))
+    return out
+
+
+def partition_slice(ops, P: int, p_begin: int, p_end: int, out: Parts = None, stream=None) -> Parts:
+    """nacho_partition_slice: boundaries p_begin .. p_end of the P-partition (a device's share)."""
+    arr = _matrices(ops)
+    out = out or Parts(p_end - p_begin, len(ops), ops[0].pos.device)
+    pc = out.c()
+    _check(lib.nacho_partition_slice(arr, len(ops), P, p_begin, ctypes.byref(pc), _stream(stream)))
     return out
 
 

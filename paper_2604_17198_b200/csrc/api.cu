@@ -142,18 +142,21 @@ nacho_status check_parts(const nacho_parts* p, int32_t k) {
   return NACHO_SUCCESS;
 }
 
-nacho_status launch_partition(const nacho_matrix* ops, int32_t k, const PartsArg& pa, cudaStream_t st) {
+// Boundaries p0 .. p0 + pa.P of the Ptot-partition into pa (whole partition: p0 = 0, Ptot = pa.P).
+nacho_status launch_partition(const nacho_matrix* ops, int32_t k, const PartsArg& pa, cudaStream_t st,
+                              int64_t Ptot = -1, int64_t p0 = 0) {
   const OpsArg a = make_ops(ops, k);
+  if (Ptot < 0) Ptot = pa.P;
+  const int64_t q = total_cost(ops, k);
   if (k == 1) {
-    partition1_kernel<<<(unsigned)((int64_t(pa.P) + 256) / 256), 256, 0, st>>>(a, pa, total_cost(ops, k));
+    partition1_kernel<<<(unsigned)((int64_t(pa.P) + 256) / 256), 256, 0, st>>>(a, pa, q, Ptot, p0);
     return launched("partition1_kernel");
   }
   const int64_t nb = (int64_t(pa.P) + 1 + kPartWarps - 1) / kPartWarps;
-  const int64_t q = total_cost(ops, k);
-  if (k == 2) partition_kernel<kPartWarps, 2><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q);
-  else if (k == 3) partition_kernel<kPartWarps, 3><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q);
-  else if (k == 4) partition_kernel<kPartWarps, 4><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q);
-  else partition_kernel<kPartWarps, NACHO_MAX_K><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q);
+  if (k == 2) partition_kernel<kPartWarps, 2><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q, Ptot, p0);
+  else if (k == 3) partition_kernel<kPartWarps, 3><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q, Ptot, p0);
+  else if (k == 4) partition_kernel<kPartWarps, 4><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q, Ptot, p0);
+  else partition_kernel<kPartWarps, NACHO_MAX_K><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q, Ptot, p0);
   return launched("partition_kernel");
 }
 
@@ -363,6 +366,16 @@ nacho_status nacho_partition(const nacho_matrix* ops, int32_t k, int32_t P, nach
   NACHO_TRY(check_parts(out, k));
   if (out->P != P) return fail(NACHO_ERR_INVALID_ARG, "parts.P = %d != P = %d", out->P, P);
   return launch_partition(ops, k, parts_arg(out), static_cast<cudaStream_t>(stream));
+}
+
+nacho_status nacho_partition_slice(const nacho_matrix* ops, int32_t k, int32_t P, int32_t p_begin, nacho_parts* out,
+                                   void* stream) {
+  NACHO_TRY(check_ops(ops, k));
+  if (P < 1) return fail(NACHO_ERR_INVALID_ARG, "P = %d < 1", P);
+  NACHO_TRY(check_parts(out, k));
+  if (p_begin < 0 || (int64_t)p_begin + out->P > P)
+    return fail(NACHO_ERR_INVALID_ARG, "slice [%d, %lld] outside [0, %d]", p_begin, (long long)p_begin + out->P, P);
+  return launch_partition(ops, k, parts_arg(out), static_cast<cudaStream_t>(stream), P, p_begin);
 }
 
 int32_t nacho_auto_partitions(const nacho_matrix* ops, int32_t k, int32_t op) {

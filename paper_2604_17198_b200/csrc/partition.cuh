@@ -9,25 +9,29 @@ namespace nacho {
 // ("computed independently, and thus in parallel").
 // KM: compile-time bound on k (sizes the per-lane register arrays of the k-way search).
 template <int WARPS, int KM>
-__global__ void __launch_bounds__(WARPS * 32) partition_kernel(const __grid_constant__ OpsArg a, PartsArg out, int64_t qstar) {
-  const int64_t p = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
-  if (p > out.P) return;  // warp-uniform
+// Boundaries p0 .. p0 + out.P of the Ptot-partition go to out[0 .. out.P] (a whole partition: p0 = 0,
+// Ptot = out.P; a device slice otherwise).
+__global__ void __launch_bounds__(WARPS * 32) partition_kernel(const __grid_constant__ OpsArg a, PartsArg out, int64_t qstar,
+                                                               int64_t Ptot, int64_t p0) {
+  const int64_t i = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (i > out.P) return;  // warp-uniform
+  const int64_t p = p0 + i;
   Boundary b;
   if (p == 0) set_origin(a, b);
-  else if (p == out.P) set_end(a, b);
-  else b = warp_find_boundary<KM>(a, query_of(qstar, out.P, p), 0, a.op[0].nouter);
+  else if (p == Ptot) set_end(a, b);
+  else b = warp_find_boundary<KM>(a, query_of(qstar, Ptot, p), 0, a.op[0].nouter);
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
-    out.query[p] = query_of(qstar, out.P, p);
-    out.row[p] = b.row;
-    out.row_pos[p] = b.row_pos;
-    out.col[p] = b.col;
+    out.query[i] = query_of(qstar, Ptot, p);
+    out.row[i] = b.row;
+    out.row_pos[i] = b.row_pos;
+    out.col[i] = b.col;
   }
   if (lane < a.k) {
     int64_t v = 0;
 #pragma unroll
     for (int o = 0; o < NACHO_MAX_K; ++o) if (o == lane) v = b.pos[o];
-    out.pos[p * a.k + lane] = v;
+    out.pos[i * a.k + lane] = v;
   }
 }
 
@@ -35,16 +39,17 @@ __global__ void __launch_bounds__(WARPS * 32) partition_kernel(const __grid_cons
 // a single compressed operand: pos = Q_p), so only the row level needs a search --
 // one thread per boundary, binary search for the largest outer position x with pos[x] <= Q_p.
 __global__ void __launch_bounds__(256) partition1_kernel(const __grid_constant__ OpsArg a, PartsArg out,
-                                                         int64_t qstar) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p > out.P) return;
+                                                         int64_t qstar, int64_t Ptot, int64_t p0) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > out.P) return;
+  const int64_t p = p0 + i;
   const OpView& A = a.op[0];
-  const int64_t Q = query_of(qstar, out.P, p);
+  const int64_t Q = query_of(qstar, Ptot, p);
   int64_t row, rp, pos;
   int32_t col = 0;
   if (p == 0) {
     row = 0; rp = 0; pos = 0;                                         // origin (R1)
-  } else if (p == out.P || Q >= A.nnz) {
+  } else if (p == Ptot || Q >= A.nnz) {
     row = a.nrows; rp = A.nouter; pos = A.nnz;                        // end (R1, R2)
   } else {
     int64_t lo = 0, hi = A.nouter;                                    // pos[lo] <= Q < pos[hi+1]
@@ -57,11 +62,11 @@ __global__ void __launch_bounds__(256) partition1_kernel(const __grid_constant__
     pos = Q;
     col = ldg(A.crd + Q);
   }
-  out.query[p] = Q;
-  out.row[p] = row;
-  out.row_pos[p] = rp;
-  out.col[p] = col;
-  out.pos[p] = pos;
+  out.query[i] = Q;
+  out.row[i] = row;
+  out.row_pos[i] = rp;
+  out.col[i] = col;
+  out.pos[i] = pos;
 }
 
 }  // namespace nacho

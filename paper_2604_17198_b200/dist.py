@@ -180,15 +180,34 @@ def spadd_assemble(nrows: int, z_pos_local: torch.Tensor, z_crd_local: torch.Ten
     return z_pos, z_crd, z_val
 
 
-def spadd(ops, parts, group=None):
-    """Distributed k-way SpAdd on the CUDA kernels (single-read staged path on each rank's slice)."""
-    from . import spadd_k_staged
+class ShardedZ:
+    """One device's share of Z = sum_o A_o under a device-level cut: the union entries of partitions
+    [lo, hi) of the global P-partition (local CSR pieces: z_pos is valid on the owned rows
+    [own_lo, own_hi), relative to this shard's first entry)."""
+
+    def __init__(self, z_pos, z_crd, z_val, nnz, own_lo, own_hi, part_off):
+        self.z_pos, self.z_crd, self.z_val = z_pos, z_crd, z_val
+        self.nnz, self.own_lo, self.own_hi, self.part_off = nnz, own_lo, own_hi, part_off
+
+
+def spadd_shard(ops, P_total: int, world: int, rank: int, out=None, ws=None, sync=True) -> ShardedZ:
+    """This device's share of the k-way SpAdd: it searches only its own P_l + 1 boundaries
+    (nacho_partition_slice) and runs the staged single-read kernels on them; no communication.
+    sync=False skips the one device->host read (nnz of the shard) for timed loops."""
+    from . import partition_slice, spadd_k_staged
+    lo, hi = rank_range(P_total, world, rank)
+    parts = partition_slice(ops, P_total, lo, hi)
+    dev = ops[0].pos.device
+    part_off = torch.empty(parts.P + 1, dtype=torch.int64, device=dev)
+    z_pos, z_crd, z_val = spadd_k_staged(ops, parts, *(out or ()), part_off=part_off, ws=ws)
+    nnz = int(part_off[-1].item()) if sync else -1
+    own_lo, own_hi = (int(parts.row[0].item()), int(parts.row[-1].item())) if sync else (-1, -1)
+    return ShardedZ(z_pos, z_crd, z_val, nnz, own_lo, own_hi, part_off)
+
+
+def spadd(ops, P_total: int, group=None):
+    """Distributed k-way SpAdd: every rank computes its shard (spadd_shard), then the Z segments are
+    all-gathered and rebased (spadd_assemble) -- equal coordinates never straddle a cut."""
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    lo, hi = rank_range(parts.P, world, rank)
-    view = slice_parts(parts, lo, hi)
-    part_off = torch.empty(view.P + 1, dtype=torch.int64, device=ops[0].pos.device)
-    z_pos, z_crd, z_val = spadd_k_staged(ops, view, part_off=part_off)
-    nnz_local = int(part_off[-1].item())
-    own_lo = int(parts.row[lo].item())
-    own_hi = int(parts.row[hi].item())
-    return spadd_assemble(ops[0].nrows, z_pos, z_crd, z_val, nnz_local, own_lo, own_hi, group=group)
+    sh = spadd_shard(ops, P_total, world, rank)
+    return spadd_assemble(ops[0].nrows, sh.z_pos, sh.z_crd, sh.z_val, sh.nnz, sh.own_lo, sh.own_hi, group=group)
