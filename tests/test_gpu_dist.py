@@ -56,3 +56,17 @@ def test_spadd_device_slices(ndev, path):
     assert np.array_equal(zp.cpu().numpy(), rp)
     assert np.array_equal(zc.cpu().numpy(), rc)
     assert np.array_equal(zv.cpu().numpy(), rv)
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_partition_slice_equals_full(k):
+    """nacho_partition_slice writes exactly the boundaries nacho_partition writes at those indices."""
+    wl = W.build("c2", 0.02, device="cuda", values="int", kmax=8)
+    ops = wl.ops[:k]
+    P = 8 * (N.auto_partitions(ops, "spadd") // 8 + 1)
+    full = N.partition(ops, P)
+    for lo, hi in ((0, P // 8), (3 * P // 8, P // 2), (7 * P // 8, P), (0, P)):
+        sl = N.partition_slice(ops, P, lo, hi)
+        for f in ("query", "row", "row_pos", "col"):
+            assert torch.equal(getattr(sl, f), getattr(full, f)[lo:hi + 1]), f
+        assert torch.equal(sl.pos, full.pos[lo * k:(hi + 1) * k])
