@@ -195,6 +195,7 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
                     kernel_bytes={"spadd_staged": algo, "partition_slice": (lparts.P + 1) * (8 * k + 28)},
                     two_pass={}, dtype="f32" if vs == 4 else "f64", wl=wl, parts=lparts,
                     exchange_ms=statistics.median(ex_ms), best="spadd_staged")
+    P = N.auto_partitions(ops, "spadd")
     parts = N.Parts(P, k, ops[0].pos.device)
     local = parts
     part_off = torch.empty(local.P + 1, dtype=torch.int64, device="cuda")
