@@ -16,13 +16,14 @@ __global__ void __launch_bounds__(WARPS * 32) partition_kernel(const __grid_cons
   const int64_t i = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (i > out.P) return;  // warp-uniform
   const int64_t p = p0 + i;
+  const int64_t Q = query_of(qstar, Ptot, p);   // one 64-bit division pair per boundary
   Boundary b;
   if (p == 0) set_origin(a, b);
   else if (p == Ptot) set_end(a, b);
-  else b = warp_find_boundary<KM>(a, query_of(qstar, Ptot, p), 0, a.op[0].nouter);
+  else b = warp_find_boundary<KM>(a, Q, 0, a.op[0].nouter);
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
-    out.query[i] = query_of(qstar, Ptot, p);
+    out.query[i] = Q;
     out.row[i] = b.row;
     out.row_pos[i] = b.row_pos;
     out.col[i] = b.col;
