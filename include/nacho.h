@@ -69,6 +69,10 @@ typedef struct {
   int64_t* row_pos;  /* [P+1]  outer-level position of x_i (CSR: == row; DCSR: index into outer_crd) */
   int32_t* col;      /* [P+1]  boundary column coordinate x_j                          (Alg. 1) */
   int64_t* pos;      /* [(P+1)*k] pos[p*k+o] = #entries of operand o before b_p        (P:1795 p.ipA) */
+  int64_t max_work;  /* host-side bound on any partition's work (entries over the operands): written by
+                        nacho_partition / nacho_partition_slice as ceil(Q* / P) + k - 1 (Theorem 1,
+                        P:1146-1161); 0 = unknown -- calls that need it then read the record's first and
+                        last query (a synchronising 16-byte copy) */
 } nacho_parts;
 
 /* ------------------------------------------------------------------------------------------------

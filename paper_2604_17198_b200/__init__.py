@@ -39,7 +39,7 @@ class Matrix(ctypes.Structure):
 class PartsC(ctypes.Structure):
     _fields_ = [("P", ctypes.c_int32), ("k", ctypes.c_int32), ("query", ctypes.c_void_p),
                 ("row", ctypes.c_void_p), ("row_pos", ctypes.c_void_p), ("col", ctypes.c_void_p),
-                ("pos", ctypes.c_void_p)]
+                ("pos", ctypes.c_void_p), ("max_work", ctypes.c_int64)]
 
 
 def _load():
@@ -141,12 +141,14 @@ class Parts:
         self.row_pos = torch.empty(P + 1, dtype=torch.int64, device=device)
         self.col = torch.empty(P + 1, dtype=torch.int32, device=device)
         self.pos = torch.empty((P + 1) * k, dtype=torch.int64, device=device)
+        self.max_work = 0   # set by partition() / partition_slice() (host-side bound, no device read)
 
     def c(self) -> PartsC:
         s = PartsC()
         s.P, s.k = self.P, self.k
         s.query, s.row, s.row_pos = self.query.data_ptr(), self.row.data_ptr(), self.row_pos.data_ptr()
         s.col, s.pos = self.col.data_ptr(), self.pos.data_ptr()
+        s.max_work = self.max_work
         return s
 
 
@@ -168,6 +170,7 @@ def partition(ops, P: int, out: Parts = None, stream=None) -> Parts:
     out = out or Parts(P, len(ops), ops[0].pos.device)
     pc = out.c()
     _check(lib.nacho_partition(arr, len(ops), P, ctypes.byref(pc), _stream(stream)))
+    out.max_work = pc.max_work
     return out
 
 
@@ -177,6 +180,7 @@ def partition_slice(ops, P: int, p_begin: int, p_end: int, out: Parts = None, st
     out = out or Parts(p_end - p_begin, len(ops), ops[0].pos.device)
     pc = out.c()
     _check(lib.nacho_partition_slice(arr, len(ops), P, p_begin, ctypes.byref(pc), _stream(stream)))
+    out.max_work = pc.max_work
     return out
 
 

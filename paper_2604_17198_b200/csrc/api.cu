@@ -117,6 +117,7 @@ PartsArg carve_parts(void* ws, int64_t P, int k) {
   PartsArg pa;
   pa.P = (int32_t)P;
   pa.k = k;
+  pa.max_work = 0;
   pa.query = reinterpret_cast<int64_t*>(c); c += align_up((P + 1) * 8);
   pa.row = reinterpret_cast<int64_t*>(c); c += align_up((P + 1) * 8);
   pa.row_pos = reinterpret_cast<int64_t*>(c); c += align_up((P + 1) * 8);
@@ -128,7 +129,7 @@ PartsArg carve_parts(void* ws, int64_t P, int k) {
 PartsArg parts_arg(const nacho_parts* p) {
   PartsArg pa;
   pa.P = p->P; pa.k = p->k; pa.query = p->query; pa.row = p->row; pa.row_pos = p->row_pos;
-  pa.col = p->col; pa.pos = p->pos;
+  pa.col = p->col; pa.pos = p->pos; pa.max_work = p->max_work;
   return pa;
 }
 
@@ -245,6 +246,7 @@ nacho_status launch_spadd4(const Spadd4Args<T>& a, cudaStream_t st) {
 // device cuts of dist.py) has a smaller span: when the cheap bound fails, the span is read from the
 // record's first and last query (a synchronising 16-byte copy).
 int64_t max_part_work(const nacho_matrix* ops, int32_t k, const PartsArg& pa, int64_t limit, cudaStream_t st) {
+  if (pa.max_work > 0) return pa.max_work;   // recorded by the partition call: no device read
   const int64_t q = total_cost(ops, k);
   int64_t w = (q + pa.P - 1) / pa.P + (k - 1);
   if (w <= limit || pa.P < 1) return w;
@@ -365,6 +367,7 @@ nacho_status nacho_partition(const nacho_matrix* ops, int32_t k, int32_t P, nach
   if (P < 1) return fail(NACHO_ERR_INVALID_ARG, "P = %d < 1", P);
   NACHO_TRY(check_parts(out, k));
   if (out->P != P) return fail(NACHO_ERR_INVALID_ARG, "parts.P = %d != P = %d", out->P, P);
+  out->max_work = (total_cost(ops, k) + P - 1) / P + (k - 1);
   return launch_partition(ops, k, parts_arg(out), static_cast<cudaStream_t>(stream));
 }
 
@@ -375,6 +378,7 @@ nacho_status nacho_partition_slice(const nacho_matrix* ops, int32_t k, int32_t P
   NACHO_TRY(check_parts(out, k));
   if (p_begin < 0 || (int64_t)p_begin + out->P > P)
     return fail(NACHO_ERR_INVALID_ARG, "slice [%d, %lld] outside [0, %d]", p_begin, (long long)p_begin + out->P, P);
+  out->max_work = (total_cost(ops, k) + P - 1) / P + (k - 1);
   return launch_partition(ops, k, parts_arg(out), static_cast<cudaStream_t>(stream), P, p_begin);
 }
 

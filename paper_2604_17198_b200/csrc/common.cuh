@@ -38,6 +38,7 @@ struct PartsArg {
   int64_t* row_pos;
   int32_t* col;
   int64_t* pos;
+  int64_t max_work;   // host-side bound (nacho_parts.max_work), 0 = unknown
 };
 
 // Q_p = floor(p * Q* / P) without 128-bit arithmetic: (Q*/P)*p + ((Q*%P)*p)/P is exact because

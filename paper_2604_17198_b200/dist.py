@@ -34,6 +34,7 @@ class PartsView:
     row_pos: torch.Tensor
     col: torch.Tensor
     pos: torch.Tensor
+    max_work: int = 0
 
     def c(self):
         from . import PartsC
@@ -41,6 +42,7 @@ class PartsView:
         s.P, s.k = self.P, self.k
         s.query, s.row, s.row_pos = self.query.data_ptr(), self.row.data_ptr(), self.row_pos.data_ptr()
         s.col, s.pos = self.col.data_ptr(), self.pos.data_ptr()
+        s.max_work = self.max_work
         return s
 
 
@@ -48,7 +50,7 @@ def slice_parts(parts, lo: int, hi: int) -> PartsView:
     """Partitions [lo, hi) of `parts` (boundaries lo..hi inclusive) without copying."""
     k = parts.k
     return PartsView(hi - lo, k, parts.query[lo:hi + 1], parts.row[lo:hi + 1], parts.row_pos[lo:hi + 1],
-                     parts.col[lo:hi + 1], parts.pos[lo * k:(hi + 1) * k])
+                     parts.col[lo:hi + 1], parts.pos[lo * k:(hi + 1) * k], getattr(parts, "max_work", 0))
 
 
 def rank_range(P_total: int, world: int, rank: int):
