@@ -29,7 +29,6 @@ struct SpaddShared {
 template <int THREADS, int SPT>
 __device__ __forceinline__ void block_max_scan(uint64_t* v, int n, uint64_t* red) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  constexpr int W = THREADS / 32;
   uint64_t loc[SPT];
   uint64_t run = 0;
 #pragma unroll

@@ -78,7 +78,6 @@ template <typename T, int V, bool DY>
 __device__ __forceinline__ void sv3_tail(const SpmvArgs<T>& a, int p, int64_t s, int n, int64_t rp0, int64_t rpE,
                                          int lim_r, bool smem_rows, const int32_t* send, T* sprod, uint8_t* mark,
                                          FV<T>* s_wagg, T* s_cin, int32_t* s_ffl) {
-  constexpr int W = kSv3Threads / 32;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t* __restrict__ gend = a.pos + rp0 + 1;
   auto row_end = [&](int r) -> int32_t { return smem_rows ? send[r] : (int32_t)(ldg(gend + r) - s); };
