@@ -31,7 +31,7 @@ typedef enum {
   NACHO_ERR_INVALID_ARG = 1, /* null pointer, P < 1, k outside [1, NACHO_MAX_K], unsupported dtype/format */
   NACHO_ERR_SHAPE = 2,       /* operand shapes disagree (k-way ops), or x / B do not match A */
   NACHO_ERR_FORMAT = 3,      /* nacho_validate found a violated sorted-level invariant */
-  NACHO_ERR_OVERFLOW = 4,    /* ncols > INT32_MAX, or a count does not fit the index types */
+  NACHO_ERR_OVERFLOW = 4,    /* nrows or ncols > INT32_MAX, or a count does not fit the index types */
   NACHO_ERR_WORKSPACE = 5,   /* ws_bytes smaller than the *_workspace_size() result */
   NACHO_ERR_CUDA = 6         /* a launch or CUDA runtime call failed */
 } nacho_status;

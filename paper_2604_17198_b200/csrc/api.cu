@@ -62,7 +62,7 @@ nacho_status check_matrix(const nacho_matrix* A, const char* name) {
   if (A->dtype != NACHO_F32 && A->dtype != NACHO_F64) return fail(NACHO_ERR_INVALID_ARG, "%s: bad dtype %d", name, A->dtype);
   if (A->nrows < 0 || A->ncols < 0 || A->nnz < 0 || A->nouter < 0) return fail(NACHO_ERR_SHAPE, "%s: negative size", name);
   if (A->ncols > INT32_MAX) return fail(NACHO_ERR_OVERFLOW, "%s: ncols %lld > INT32_MAX", name, (long long)A->ncols);
-  if (A->nrows >= (int64_t(1) << 32)) return fail(NACHO_ERR_OVERFLOW, "%s: nrows >= 2^32", name);
+  if (A->nrows > INT32_MAX) return fail(NACHO_ERR_OVERFLOW, "%s: nrows > INT32_MAX (local row spans are 32-bit)", name);
   if (A->format == NACHO_CSR && A->nouter != A->nrows) return fail(NACHO_ERR_SHAPE, "%s: CSR needs nouter == nrows", name);
   if (A->format == NACHO_DCSR && A->nouter > A->nrows) return fail(NACHO_ERR_SHAPE, "%s: DCSR nouter > nrows", name);
   if (!A->pos) return fail(NACHO_ERR_INVALID_ARG, "%s: null pos", name);
