@@ -68,4 +68,6 @@ def test_invalid_arguments_rejected_before_launch():
     assert L.nacho_partition(ctypes.byref(m), 1, 0, ctypes.byref(parts), None) in (1,)
     m.ncols = 2**31
     assert L.nacho_spmv(ctypes.byref(m), None, None, None, 0, None, 0, None) in (1, 4)
+    m = _desc(10, nrows=2**31)   # partition-local row spans are 32-bit
+    assert L.nacho_partition(ctypes.byref(m), 1, 4, ctypes.byref(parts), None) == 4
     assert b"" != L.nacho_last_error()
