@@ -326,16 +326,19 @@ template <typename T>
 nacho_status run_spadd_staged(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
                               int64_t* z_pos, int32_t* z_crd, T* z_val, char* ws, cudaStream_t st) {
   const int64_t q = total_cost(ops, k);
+  const size_t words = align_up((size_t)(parts->P + 1) * 8);
+  const int64_t nblk = ((int64_t)parts->P >> kS4BlkShift) + 1;
   int64_t* cnt = reinterpret_cast<int64_t*>(ws);
-  int32_t* t_crd = reinterpret_cast<int32_t*>(ws + align_up((size_t)(parts->P + 1) * 8));
+  auto* blk = reinterpret_cast<unsigned long long*>(ws + words);
+  int32_t* t_crd = reinterpret_cast<int32_t*>(ws + 2 * words);
   T* t_val = reinterpret_cast<T*>(reinterpret_cast<char*>(t_crd) + align_up((size_t)q * 4));
-  Spadd4Args<T> a{make_ops(ops, k), parts_arg(parts), cnt, part_off, nullptr, nullptr, z_pos, t_crd, t_val};
+  if (cudaMemsetAsync(blk, 0, sizeof(unsigned long long) * nblk, st) != cudaSuccess)
+    return fail(NACHO_ERR_CUDA, "memset block sums");
+  Spadd4Args<T> a{make_ops(ops, k), parts_arg(parts), cnt, part_off, nullptr, nullptr, z_pos, t_crd, t_val, blk};
   NACHO_TRY((launch_spadd4<T, kS4Stage>(a, st)));
-  scan_counts_kernel<1024><<<1, 1024, 0, st>>>(cnt, parts->P, part_off);
-  NACHO_TRY(launched("scan_counts_kernel"));
-  Spadd4Args<T> c{make_ops(ops, k), parts_arg(parts), nullptr, part_off, nullptr, nullptr, z_pos, z_crd, z_val};
-  s4_compact_kernel<T><<<(unsigned)parts->P, kS4Threads, 0, st>>>(c, t_crd, t_val);
-  return launched("s4_compact_kernel");
+  Spadd4Args<T> c{make_ops(ops, k), parts_arg(parts), cnt, part_off, nullptr, nullptr, z_pos, z_crd, z_val, blk};
+  s4_place_kernel<T><<<(unsigned)parts->P, kS4Threads, 0, st>>>(c, t_crd, t_val);
+  return launched("s4_place_kernel");
 }
 
 }  // namespace
@@ -513,7 +516,7 @@ size_t nacho_spadd_k_staged_workspace_size(const nacho_matrix* ops, int32_t k, i
   if (!ops || k < 1) return 0;
   const int64_t q = total_cost(ops, k);
   const size_t vs = ops[0].dtype == NACHO_F64 ? 8 : 4;
-  return align_up((size_t)((P > 0 ? P : 1) + 1) * 8) + align_up((size_t)q * 4) + align_up((size_t)q * vs);
+  return 2 * align_up((size_t)((P > 0 ? P : 1) + 1) * 8) + align_up((size_t)q * 4) + align_up((size_t)q * vs);
 }
 
 /* Single read of the operands, no look-back: staged union + scan + placement (spadd4.cuh). */

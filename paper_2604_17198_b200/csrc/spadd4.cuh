@@ -26,7 +26,7 @@ namespace nacho {
 
 // kS4Stage: single read of the operands without a look-back -- the union goes to a staging buffer at
 // the partition's provisional offset sum_o b_p.pos[o] (>= its final one), Z.pos gets partition-local
-// counts, cnt[p] = union size; scan_counts + s4_compact_kernel then place it.
+// counts, cnt[p] = union size (and per-block sums); s4_place_kernel then places it.
 enum S4Mode { kS4Count = 0, kS4Fill = 1, kS4Fused = 2, kS4Stage = 3 };
 
 // Phase timers (debug build -DNACHO_PROF): thread 0 of every 16th partition adds its clock64 deltas.
@@ -59,6 +59,7 @@ constexpr int kS4Threads = NACHO_S4_THREADS;
 constexpr int kS4Vt = NACHO_S4_VT;                // merged entries per thread and stage
 constexpr int kS4Tile = kS4Threads * kS4Vt;       // entries per partition
 constexpr int kS4Buf = kS4Tile + kS4Tile / 16 + 8;   // padded stage-buffer capacity (elements)
+constexpr int kS4BlkShift = 8;                    // kS4Stage: partitions per block sum = 256
 constexpr int kS4DenseWords = 2048;               // widest column range of the bitmap path (x 32 columns)
 constexpr int kS4PosRound = 8;                    // row pointers loaded per thread and round
 
@@ -73,6 +74,7 @@ struct Spadd4Args {
   int64_t* z_pos;
   int32_t* z_crd;
   T* z_val;
+  unsigned long long* blk_cnt;    // kS4Stage: union sizes summed per block of 2^kS4BlkShift partitions
 };
 
 // Padded slot of element i of a thread-blocked stage buffer (conflict-free blocked accesses).
@@ -581,7 +583,7 @@ __device__ __forceinline__ void s4_dense(const Spadd4Args<T>& a, SH& sh, int64_t
 #pragma unroll
     for (int o = 0; o < KM; ++o) if (o < k) off += sh.b0pos[o];
     pos_off = 0;
-    if (tid == 0) a.part_cnt[p] = nu;
+    if (tid == 0) { a.part_cnt[p] = nu; atomicAdd(a.blk_cnt + (p >> kS4BlkShift), (unsigned long long)nu); }
   } else {
     if (w == 0) {
       const int64_t ex = s4_lookback(a.lb_state, p, nu);
@@ -689,7 +691,10 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, SH& sh, int64_t 
     }
     if (p == 0 && tid == 0) a.z_pos[0] = 0;
     const int nu = s4_union_emit<T, KT, KIND, SH>(sh, k, K, Z1, Z2, S1, S2, out);
-    if (MODE == kS4Stage && tid == 0) a.part_cnt[p] = nu;
+    if (MODE == kS4Stage && tid == 0) {
+      a.part_cnt[p] = nu;
+      atomicAdd(a.blk_cnt + (p >> kS4BlkShift), (unsigned long long)nu);
+    }
     S4PH(4);
     return;
   }
@@ -912,34 +917,55 @@ __global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 1280 / kS4Thr
 }
 
 // Places the staged unions (kS4Stage): partition p's union moves from its provisional offset
-// sum_o b_p.pos[o] to part_off[p], and its owned Z.pos entries (rows [b_p.row, b_{p+1}.row)) get
-// part_off[p] added.  One CTA per partition; coalesced copies.
+// sum_o b_p.pos[o] to its final offset, and its owned Z.pos entries (rows [b_p.row, b_{p+1}.row)) get
+// that offset added.  The offset -- the exclusive prefix of the union sizes -- is computed
+// here from the per-256-partition block sums the stage kernel accumulated plus the sizes of p's
+// predecessors inside its block (no separate scan kernel).  One CTA per partition.
 template <typename T>
-__global__ void __launch_bounds__(kS4Threads) s4_compact_kernel(const __grid_constant__ Spadd4Args<T> a,
-                                                                 const int32_t* __restrict__ t_crd,
-                                                                 const T* __restrict__ t_val) {
+__global__ void __launch_bounds__(kS4Threads) s4_place_kernel(const __grid_constant__ Spadd4Args<T> a,
+                                                               const int32_t* __restrict__ t_crd,
+                                                               const T* __restrict__ t_val) {
+  __shared__ unsigned long long s_red[kS4Threads / 32];
   const int64_t p = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t b = p >> kS4BlkShift;
+  unsigned long long v = 0;
+  for (int64_t i = tid; i < b; i += kS4Threads) v += a.blk_cnt[i];
+  const int64_t q = (b << kS4BlkShift) + tid;
+  if (q < p) v += (unsigned long long)ldg(a.part_cnt + q);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+  if (lane == 0) s_red[w] = v;
+  __syncthreads();
+  unsigned long long tot = 0;
+#pragma unroll
+  for (int ww = 0; ww < kS4Threads / 32; ++ww) tot += s_red[ww];
+  const int64_t off = (int64_t)tot;
+  const int64_t nu = ldg(a.part_cnt + p);
+  if (tid == 0) {
+    a.part_off[p] = off;
+    if (p == a.parts.P - 1) a.part_off[a.parts.P] = off + nu;
+  }
   const int k = a.ops.k;
   int64_t prov = 0;
   for (int o = 0; o < k; ++o) prov += ldg(a.parts.pos + p * k + o);
-  const int64_t off = ldg(a.part_off + p), nu = ldg(a.part_off + p + 1) - off;
   constexpr int U = 4;   // loads in flight per thread
   for (int64_t jb = 0; jb < nu; jb += U * kS4Threads) {
     int32_t c[U];
-    T v[U];
+    T vv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t j = jb + u * kS4Threads + threadIdx.x;
-      if (j < nu) { c[u] = __ldcs(t_crd + prov + j); v[u] = __ldcs(t_val + prov + j); }
+      const int64_t j = jb + u * kS4Threads + tid;
+      if (j < nu) { c[u] = __ldcs(t_crd + prov + j); vv[u] = __ldcs(t_val + prov + j); }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t j = jb + u * kS4Threads + threadIdx.x;
-      if (j < nu) { a.z_crd[off + j] = c[u]; a.z_val[off + j] = v[u]; }
+      const int64_t j = jb + u * kS4Threads + tid;
+      if (j < nu) { a.z_crd[off + j] = c[u]; a.z_val[off + j] = vv[u]; }
     }
   }
   const int64_t r0 = ldg(a.parts.row + p), r1 = ldg(a.parts.row + p + 1);
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += kS4Threads) a.z_pos[r + 1] += off;
+  for (int64_t r = r0 + tid; r < r1; r += kS4Threads) a.z_pos[r + 1] += off;
 }
 
 }  // namespace nacho
