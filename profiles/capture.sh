@@ -16,7 +16,7 @@ if [ "${PART:-1}" = "1" ]; then
       > /dev/null 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"spadd4_kernel|partition_kernel" -s 4 -c 3 \
       -o gpurun_out/full_c2 -f python profiles/run_once.py c2 --steps 3 > gpurun_out/ncu_full_c2.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"spadd4_kernel|s4_compact" -s 0 -c 2 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"spadd4_kernel|s4_place" -s 0 -c 2 \
       -o gpurun_out/full_c2_staged -f python profiles/run_staged.py > gpurun_out/ncu_full_c2_staged.log 2>&1
 else
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spmv3_kernel" -s 1 -c 1 \
