@@ -43,9 +43,6 @@ nacho_status launched(const char* what) {
     if (_s != NACHO_SUCCESS) return _s;       \
   } while (0)
 
-constexpr int kSpmvThreads = 256;
-constexpr int kSpmvIptF32 = 16;   // 4096 positions per CTA
-constexpr int kSpmvIptF64 = 8;    // 2048
 constexpr int kSpaddThreads = 256;
 constexpr int kSpaddTile = 2048;  // entries (summed over operands) per CTA chunk
 constexpr int kSpmmWarps = 8;
@@ -161,6 +158,14 @@ nacho_status launch_partition(const nacho_matrix* ops, int32_t k, const PartsArg
   return launched("partition_kernel");
 }
 
+// Carries of an SpMV over P partitions made by nacho_partition (work <= ceil(nnz / P)): one per
+// tile-sized chunk.
+int64_t spmv_carry_cap(const nacho_matrix* A, int64_t P) {
+  const int64_t tile = A->dtype == NACHO_F64 ? sv3_tile<double>() : sv3_tile<float>();
+  const int64_t w = (A->nnz + P - 1) / P;
+  return P * (w <= tile ? 1 : (w + tile - 1) / tile);
+}
+
 int32_t auto_p(int64_t work, int64_t tile) {
   int64_t P = (work + tile - 1) / tile;
   if (P < 1) P = 1;
@@ -170,7 +175,7 @@ int32_t auto_p(int64_t work, int64_t tile) {
 
 template <typename T>
 nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, void* y, int32_t dense_y,
-                      char* ws_carry, cudaStream_t st) {
+                      char* ws_carry, int64_t carry_cap, cudaStream_t st) {
   SpmvArgs<T> a;
   a.pos = A->pos; a.crd = A->crd; a.val = static_cast<const T*>(A->val);
   a.outer = A->format == NACHO_DCSR ? A->outer_crd : nullptr;
@@ -178,23 +183,24 @@ nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, 
   a.ncols = A->ncols;
   a.x = static_cast<const T*>(x); a.y = static_cast<T*>(y);
   a.dense_y = (A->format == NACHO_DCSR && dense_y) ? 1 : 0;
-  a.P = pa.P; a.ppos = pa.pos; a.prow = pa.row_pos;
+  a.ppos = pa.pos; a.prow = pa.row_pos;
+  // partitions larger than a tile run as tile-sized chunks (one CTA each, spmv3.cuh)
+  const int64_t maxpart = max_part_work(A, 1, pa, sv3_tile<T>(), st);
+  const int64_t chunks = maxpart <= sv3_tile<T>() ? 1 : (maxpart + sv3_tile<T>() - 1) / sv3_tile<T>();
+  if (int64_t(pa.P) * chunks > carry_cap)
+    return fail(NACHO_ERR_WORKSPACE, "partitions of up to %lld positions need %lld carries, workspace holds %lld",
+                (long long)maxpart, (long long)(int64_t(pa.P) * chunks), (long long)carry_cap);
+  a.chunks = (int32_t)chunks;
+  a.P = (int32_t)(int64_t(pa.P) * chunks);
   a.carry_row = reinterpret_cast<int64_t*>(ws_carry);
-  a.carry_val = reinterpret_cast<T*>(ws_carry + align_up(int64_t(pa.P) * 8));
+  a.carry_val = reinterpret_cast<T*>(ws_carry + align_up(carry_cap * 8));
   if (a.dense_y) {
     if (cudaMemsetAsync(y, 0, sizeof(T) * A->nrows, st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "memset y");
   }
-  const int64_t maxpart = max_part_work(A, 1, pa, sv3_tile<T>(), st);
-  if (maxpart <= sv3_tile<T>()) {  // register-streaming kernel, one CTA per partition (spmv3.cuh)
-    if (a.dense_y) spmv3_kernel<T, true><<<pa.P, kSv3Threads, 0, st>>>(a);
-    else spmv3_kernel<T, false><<<pa.P, kSv3Threads, 0, st>>>(a);
-    NACHO_TRY(launched("spmv3_kernel"));
-  } else {
-    if constexpr (sizeof(T) == 8) spmv_kernel<T, kSpmvThreads, kSpmvIptF64><<<pa.P, kSpmvThreads, 0, st>>>(a);
-    else spmv_kernel<T, kSpmvThreads, kSpmvIptF32><<<pa.P, kSpmvThreads, 0, st>>>(a);
-    NACHO_TRY(launched("spmv_kernel"));
-  }
-  const int64_t warps = (pa.P + 31) / 32;
+  if (a.dense_y) spmv3_kernel<T, true><<<(unsigned)a.P, kSv3Threads, 0, st>>>(a);
+  else spmv3_kernel<T, false><<<(unsigned)a.P, kSv3Threads, 0, st>>>(a);
+  NACHO_TRY(launched("spmv3_kernel"));
+  const int64_t warps = (int64_t(a.P) + 31) / 32;
   spmv_fixup_kernel<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
   return launched("spmv_fixup_kernel");
 }
@@ -398,7 +404,8 @@ size_t nacho_spmv_workspace_size(const nacho_matrix* A, int32_t P) {
   const bool auto_parts = P <= 0;
   const int64_t Pe = auto_parts ? nacho_auto_partitions(A, 1, 0) : P;
   const size_t vs = A->dtype == NACHO_F64 ? 8 : 4;
-  return align_up(Pe * 8) + align_up(Pe * vs) + (auto_parts ? parts_bytes(Pe, 1) : 0);
+  const int64_t nc = spmv_carry_cap(A, Pe);
+  return align_up(nc * 8) + align_up(nc * vs) + (auto_parts ? parts_bytes(Pe, 1) : 0);
 }
 
 nacho_status nacho_spmv(const nacho_matrix* A, const nacho_parts* parts, const void* x, void* y, int32_t dense_y,
@@ -412,16 +419,17 @@ nacho_status nacho_spmv(const nacho_matrix* A, const nacho_parts* parts, const v
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* c = static_cast<char*>(ws);
   PartsArg pa;
+  const int64_t P = parts ? parts->P : nacho_auto_partitions(A, 1, 0);
+  const int64_t cap = spmv_carry_cap(A, P);
   if (parts) {
     pa = parts_arg(parts);
   } else {
-    const int64_t P = nacho_auto_partitions(A, 1, 0);
     const size_t vs = A->dtype == NACHO_F64 ? 8 : 4;
-    pa = carve_parts(c + align_up(P * 8) + align_up(P * vs), P, 1);
+    pa = carve_parts(c + align_up(cap * 8) + align_up(cap * vs), P, 1);
     NACHO_TRY(launch_partition(A, 1, pa, st));
   }
-  if (A->dtype == NACHO_F64) return run_spmv<double>(A, pa, x, y, dense_y, c, st);
-  return run_spmv<float>(A, pa, x, y, dense_y, c, st);
+  if (A->dtype == NACHO_F64) return run_spmv<double>(A, pa, x, y, dense_y, c, cap, st);
+  return run_spmv<float>(A, pa, x, y, dense_y, c, cap, st);
 }
 
 size_t nacho_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {

@@ -75,7 +75,7 @@ __device__ __forceinline__ FV<T> fv_op(FV<T> a, FV<T> b) { return FV<T>{a.f | b.
 // Steps 2-5 of a tile (after the products are in sprod and the row ends in send, and a barrier):
 // row-start marks, segmented scan, row sums, carry.  Ends with every smem read done (barrier).
 template <typename T, int V, bool DY>
-__device__ __forceinline__ void sv3_tail(const SpmvArgs<T>& a, int p, int64_t s, int n, int64_t rp0, int64_t rpE,
+__device__ __forceinline__ void sv3_tail(const SpmvArgs<T>& a, int64_t p, int64_t s, int n, int64_t rp0, int64_t rpE,
                                          int lim_r, bool smem_rows, const int32_t* send, T* sprod, uint8_t* mark,
                                          FV<T>* s_wagg, T* s_cin, int32_t* s_ffl) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -184,11 +184,39 @@ __global__ void __launch_bounds__(kSv3Threads, Sv3Cfg<T>::MINB) spmv3_kernel(con
   __shared__ int32_t s_ffl[kSv3Threads];       // thread t's first flagged item (or its end)
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int p = blockIdx.x;
-  const int64_t s = ldg(a.ppos + p), e = ldg(a.ppos + p + 1);
-  const int64_t rp0 = ldg(a.prow + p), rpE = ldg(a.prow + p + 1);
-  const int n = (int)(e - s);                  // positions of this partition (<= SLOTS)
-  const int wb = w * WCH;                      // warp chunk [wb, wb + WCH) in local positions
+  // CTA = chunk c of partition p: a partition larger than a tile is processed as tile-sized chunks,
+  // each a sub-partition cut in position space (the single-operand cut of P:1735-1737), so the
+  // carries of consecutive chunks chain exactly like those of partitions
+  const int64_t cid = blockIdx.x;
+  const int64_t p = a.chunks == 1 ? cid : cid / a.chunks;
+  const int c = (int)(cid - p * a.chunks);
+  const int64_t sp = ldg(a.ppos + p), ep = ldg(a.ppos + p + 1);
+  const int64_t rp0p = ldg(a.prow + p), rpEp = ldg(a.prow + p + 1);
+  const int64_t s = sp + (int64_t)c * SLOTS;
+  if (c > 0 && s >= ep) {   // past the partition: a zero carry keeps row rpEp's run contiguous
+    if (tid == 0) {
+      a.carry_row[cid] = rpEp < a.nouter ? rpEp : -1;
+      a.carry_val[cid] = T(0);
+    }
+    return;
+  }
+  const int64_t e = ep - s < SLOTS ? ep : s + SLOTS;
+  int64_t rp0 = rp0p, rpE = rpEp;
+  if (a.chunks > 1) {   // rows containing the chunk's cuts: 32-ary warp searches over the partition's rows
+    __shared__ int64_t s_rows[2];
+    const int64_t hi = rpEp < a.nouter ? rpEp : a.nouter;
+    if (w < 2) {
+      const int64_t q = w == 0 ? s : e;
+      const bool need = w == 0 ? c > 0 : e < ep;
+      int64_t r = w == 0 ? rp0p : rpEp;
+      if (need) r = warp_highest_true(rp0p, hi, [&](int64_t x) { return ldg(a.pos + x) <= q; });
+      if (lane == 0) s_rows[w] = r;
+    }
+    __syncthreads();
+    rp0 = s_rows[0];
+    rpE = s_rows[1];
+  }
+  const int n = (int)(e - s);  const int wb = w * WCH;                      // warp chunk [wb, wb + WCH) in local positions
   // owned rows [0, lim_r) (R7): local ends E[r] = pos[rp0 + r + 1] - s, in [0, n]
   const int lim_r = (int)((rpE < a.nouter ? rpE : a.nouter) - rp0);
   const bool smem_rows = lim_r <= ROWCAP;
@@ -205,7 +233,7 @@ __global__ void __launch_bounds__(kSv3Threads, Sv3Cfg<T>::MINB) spmv3_kernel(con
   if (smem_rows)
     for (int i = tid; i < lim_r; i += kSv3Threads) send[i] = (int32_t)(ldg(gend + i) - s);
   __syncthreads();
-  sv3_tail<T, V, DY>(a, p, s, n, rp0, rpE, lim_r, smem_rows, send, sprod, mark, s_wagg, s_cin, s_ffl);
+  sv3_tail<T, V, DY>(a, cid, s, n, rp0, rpE, lim_r, smem_rows, send, sprod, mark, s_wagg, s_cin, s_ffl);
 }
 
 }  // namespace nacho
