@@ -278,16 +278,23 @@ nacho_status launch_spmm(const SpmmArgs<T>& a, cudaStream_t st) {
 }
 
 template <typename T>
-nacho_status run_spmm(const SpmmArgs<T>& a, cudaStream_t st, int64_t nnz) {
+nacho_status run_spmm(SpmmArgs<T> a, cudaStream_t st, int64_t maxpart, int64_t carry_cap) {
+  a.chunks = 1;
   if constexpr (sizeof(T) == 4) {
     const bool al = reinterpret_cast<uintptr_t>(a.B) % 16 == 0 && reinterpret_cast<uintptr_t>(a.C) % 16 == 0 &&
                     a.ldb % 4 == 0 && a.ldc % 4 == 0;
-    if (a.nb == 64 && al && (nnz + a.P - 1) / a.P <= kSm2Tile) {  // eight-lane-group fast path
-      spmm64_kernel<<<a.P, 256, 0, st>>>(a);
-      NACHO_TRY(launched("spmm64_kernel"));
-      const int64_t warps = (a.P + 31) / 32;
-      spmm_fixup_kernel<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
-      return launched("spmm_fixup_kernel");
+    if (a.nb == 64 && al) {  // eight-lane-group fast path; larger partitions as tile-sized chunks
+      const int64_t chunks = maxpart <= kSm2Tile ? 1 : (maxpart + kSm2Tile - 1) / kSm2Tile;
+      if (int64_t(a.P) * chunks <= carry_cap) {
+        a.chunks = (int32_t)chunks;
+        a.P = (int32_t)(int64_t(a.P) * chunks);
+        if (chunks > 1) spmm64_kernel<true><<<(unsigned)a.P, 256, 0, st>>>(a);
+        else spmm64_kernel<false><<<(unsigned)a.P, 256, 0, st>>>(a);
+        NACHO_TRY(launched("spmm64_kernel"));
+        const int64_t warps = (int64_t(a.P) + 31) / 32;
+        spmm_fixup_kernel<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
+        return launched("spmm_fixup_kernel");
+      }
     }
   }
   const int cpl = a.nb <= 32 ? 1 : a.nb <= 64 ? 2 : a.nb <= 128 ? 4 : 8;
@@ -548,12 +555,19 @@ nacho_status nacho_spadd_k_staged(const nacho_matrix* ops, int32_t k, const nach
                                  static_cast<char*>(ws), st);
 }
 
+// Carries of an SpMM over P partitions made by nacho_partition: one per tile-sized chunk.
+int64_t spmm_carry_cap(const nacho_matrix* A, int64_t P) {
+  const int64_t w = (A->nnz + P - 1) / P;
+  return P * (w <= kSm2Tile ? 1 : (w + kSm2Tile - 1) / kSm2Tile);
+}
+
 size_t nacho_spmm_workspace_size(const nacho_matrix* A, int32_t P, int32_t nb) {
   if (!A) return 0;
   const bool auto_parts = P <= 0;
   const int64_t Pe = auto_parts ? nacho_auto_partitions(A, 1, 2) : P;
   const size_t vs = A->dtype == NACHO_F64 ? 8 : 4;
-  return align_up(Pe * 8) + align_up(Pe * vs * (nb > 0 ? nb : 1)) + (auto_parts ? parts_bytes(Pe, 1) : 0);
+  const int64_t nc = spmm_carry_cap(A, Pe);
+  return align_up(nc * 8) + align_up(nc * vs * (nb > 0 ? nb : 1)) + (auto_parts ? parts_bytes(Pe, 1) : 0);
 }
 
 nacho_status nacho_spmm(const nacho_matrix* A, const nacho_parts* parts, const void* B, int64_t ldb, int32_t nb,
@@ -570,22 +584,24 @@ nacho_status nacho_spmm(const nacho_matrix* A, const nacho_parts* parts, const v
   char* c = static_cast<char*>(ws);
   const int64_t P = parts ? parts->P : nacho_auto_partitions(A, 1, 2);
   const size_t vs = A->dtype == NACHO_F64 ? 8 : 4;
+  const int64_t cap = spmm_carry_cap(A, P);
   PartsArg pa;
   if (parts) pa = parts_arg(parts);
   else {
-    pa = carve_parts(c + align_up(P * 8) + align_up(P * vs * nb), P, 1);
+    pa = carve_parts(c + align_up(cap * 8) + align_up(cap * vs * nb), P, 1);
     NACHO_TRY(launch_partition(A, 1, pa, st));
   }
+  const int64_t maxpart = max_part_work(A, 1, pa, kSm2Tile, st);
   if (A->dtype == NACHO_F64) {
     SpmmArgs<double> a{A->pos, A->crd, static_cast<const double*>(A->val), A->nrows, static_cast<const double*>(B), ldb,
-                       nb, static_cast<double*>(C), ldc, pa.P, pa.pos, pa.row_pos,
-                       reinterpret_cast<int64_t*>(c), reinterpret_cast<double*>(c + align_up(P * 8))};
-    return run_spmm<double>(a, st, A->nnz);
+                       nb, static_cast<double*>(C), ldc, pa.P, 1, pa.pos, pa.row_pos,
+                       reinterpret_cast<int64_t*>(c), reinterpret_cast<double*>(c + align_up(cap * 8))};
+    return run_spmm<double>(a, st, maxpart, cap);
   }
   SpmmArgs<float> a{A->pos, A->crd, static_cast<const float*>(A->val), A->nrows, static_cast<const float*>(B), ldb,
-                    nb, static_cast<float*>(C), ldc, pa.P, pa.pos, pa.row_pos,
-                    reinterpret_cast<int64_t*>(c), reinterpret_cast<float*>(c + align_up(P * 8))};
-  return run_spmm<float>(a, st, A->nnz);
+                    nb, static_cast<float*>(C), ldc, pa.P, 1, pa.pos, pa.row_pos,
+                    reinterpret_cast<int64_t*>(c), reinterpret_cast<float*>(c + align_up(cap * 8))};
+  return run_spmm<float>(a, st, maxpart, cap);
 }
 
 nacho_status nacho_validate(const nacho_matrix* A, void* stream) {

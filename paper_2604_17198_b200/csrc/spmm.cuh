@@ -15,7 +15,8 @@ struct SpmmArgs {
   int32_t nb;
   T* C;
   int64_t ldc;
-  int32_t P;
+  int32_t P;           // carries (the fix-up's count): partitions x chunks
+  int32_t chunks;      // spmm64: CTAs per partition (tile-sized chunks of larger partitions)
   const int64_t* ppos;
   const int64_t* prow;
   int64_t* carry_row;  // [P]
@@ -204,14 +205,42 @@ constexpr int kSm2Groups = 32;       // 8-lane groups per CTA (256 threads)
 constexpr int kSm2Items = 32;        // positions per group
 constexpr int kSm2Tile = kSm2Groups * kSm2Items;
 
+template <bool CHUNKED>
 __global__ void __launch_bounds__(256, 3) spmm64_kernel(const __grid_constant__ SpmmArgs<float> a) {
   __shared__ float4 s_tail[kSm2Groups][16];   // 64 floats per group
   __shared__ int64_t s_tkey[kSm2Groups];
   const int tid = threadIdx.x, g = tid >> 3, gl = tid & 7;
   const unsigned gmask = 0xffu << (tid & 24);
-  const int p = blockIdx.x;
-  const int64_t s = ldg(a.ppos + p), e = ldg(a.ppos + p + 1);
-  const int64_t rp0 = ldg(a.prow + p), rpE = ldg(a.prow + p + 1);
+  // CTA = chunk c of partition p (partitions larger than a tile run as tile-sized chunks, cut in
+  // position space; their carries chain like those of partitions)
+  const int64_t p = blockIdx.x;   // carry index
+  const int64_t pp = CHUNKED ? p / a.chunks : p;
+  const int c = (int)(p - pp * a.chunks);
+  const int64_t sp = ldg(a.ppos + pp), ep = ldg(a.ppos + pp + 1);
+  const int64_t rp0p = ldg(a.prow + pp), rpEp = ldg(a.prow + pp + 1);
+  const int64_t s = sp + (int64_t)c * kSm2Tile;
+  if (CHUNKED && c > 0 && s >= ep) {   // past the partition: a zero carry keeps row rpEp's run contiguous
+    if (tid == 0) a.carry_row[p] = rpEp < a.nrows ? rpEp : -1;
+    if (tid < 16) reinterpret_cast<float4*>(a.carry_val + p * 64)[tid] = make_float4(0, 0, 0, 0);
+    return;
+  }
+  const int64_t e = ep - s < kSm2Tile ? ep : s + kSm2Tile;
+  int64_t rp0 = rp0p, rpE = rpEp;
+  if (CHUNKED) {
+    __shared__ int64_t s_rows[2];
+    const int w = tid >> 5, lane = tid & 31;
+    const int64_t hi = rpEp < a.nrows ? rpEp : a.nrows;
+    if (w < 2) {
+      const int64_t q = w == 0 ? s : e;
+      const bool need = w == 0 ? c > 0 : e < ep;
+      int64_t r = w == 0 ? rp0p : rpEp;
+      if (need) r = warp_highest_true(rp0p, hi, [&](int64_t x) { return ldg(a.pos + x) <= q; });
+      if (lane == 0) s_rows[w] = r;
+    }
+    __syncthreads();
+    rp0 = s_rows[0];
+    rpE = s_rows[1];
+  }
   const int i0 = g * kSm2Items;
   const int n = (int)(e - s);
   const bool active = i0 < n || g == 0;
