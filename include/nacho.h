@@ -150,10 +150,14 @@ nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts
  * final offset, the cost C(b_p) of Theorem 1, P:1151-1158) of a workspace staging buffer, with
  * partition-local Z.pos counts; an exclusive prefix sum of the union sizes (P:1475) and a placement
  * pass then move every union to part_off[p] and add part_off[p] to the Z.pos entries it owns (R7).
+ *   Partitions of any size: one larger than the 2048-entry tile runs as chunks whose cuts are
+ *   further Alg. 1 searches (queries C(b_p) + c (2048 - k + 1)), so every coordinate still lies in
+ *   one chunk (P:2635-2639) and a caller's coarse P (e.g. one partition per worker) stays fast.
  *   part_off [P+1] int64 (required; part_off[P] = nnz_Z).  z_crd / z_val: capacity >= nnz_Z (Q* is
- *   always enough).  Partitions must hold at most 2048 entries (as nacho_spadd_k).
- *   ws  >= nacho_spadd_k_staged_workspace_size(ops, k, P) bytes: (P+1) int64 counts + Q* staged
- *   (col, value) pairs.  Errors as nacho_spadd_k. */
+ *   always enough).
+ *   ws  >= nacho_spadd_k_staged_workspace_size(ops, k, P) bytes: per-chunk counts, offsets and rows +
+ *   Q* staged (col, value) pairs (sized for partitions from nacho_partition; a record whose max_work
+ *   exceeds ceil(Q*/P) + k - 1 may need more: WORKSPACE).  Errors as nacho_spadd_k. */
 size_t nacho_spadd_k_staged_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P);
 nacho_status nacho_spadd_k_staged(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
                                   int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes,

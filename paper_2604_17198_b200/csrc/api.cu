@@ -221,7 +221,7 @@ nacho_status launch_spadd(const SpaddArgs<T>& a, cudaStream_t st) {
 }
 
 template <typename T, int MODE, int KM>
-nacho_status launch_spadd4_k(const Spadd4Args<T>& a, cudaStream_t st) {
+nacho_status launch_spadd4_k(const Spadd4Args<T>& a, cudaStream_t st, int64_t grid) {
   auto kern = spadd4_kernel<T, MODE, KM>;
   const size_t smem = sizeof(S4Shared<T, s4_small(MODE, KM)>);
   static bool configured = false;
@@ -230,19 +230,20 @@ nacho_status launch_spadd4_k(const Spadd4Args<T>& a, cudaStream_t st) {
       return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(spadd4_kernel)");
     configured = true;
   }
-  kern<<<(unsigned)a.parts.P, kS4Threads, smem, st>>>(a);
+  kern<<<(unsigned)grid, kS4Threads, smem, st>>>(a);
   return launched(MODE == kS4Count ? "spadd4_count" : MODE == kS4Fill ? "spadd4_fill" : MODE == kS4Fused ? "spadd4_fused" : "spadd4_stage");
 }
 
 // One CTA per partition (spadd4.cuh); shared memory is dynamic (> 48 KB).  k = 2, 3 (and 1) get
 // compile-time operand loops; other k the generic instantiation.
 template <typename T, int MODE>
-nacho_status launch_spadd4(const Spadd4Args<T>& a, cudaStream_t st) {
+nacho_status launch_spadd4(const Spadd4Args<T>& a, cudaStream_t st, int64_t grid = -1) {
+  if (grid < 0) grid = a.parts.P;
   switch (a.ops.k) {
-    case 1: return launch_spadd4_k<T, MODE, 1>(a, st);
-    case 2: return launch_spadd4_k<T, MODE, 2>(a, st);
-    case 3: return launch_spadd4_k<T, MODE, 3>(a, st);
-    default: return launch_spadd4_k<T, MODE, NACHO_MAX_K>(a, st);
+    case 1: return launch_spadd4_k<T, MODE, 1>(a, st, grid);
+    case 2: return launch_spadd4_k<T, MODE, 2>(a, st, grid);
+    case 3: return launch_spadd4_k<T, MODE, 3>(a, st, grid);
+    default: return launch_spadd4_k<T, MODE, NACHO_MAX_K>(a, st, grid);
   }
 }
 
@@ -335,22 +336,50 @@ __global__ void validate_kernel(nacho_matrix A, int* flag) {
   if (bad) atomicMax(flag, bad);
 }
 
+// Chunks per partition of the staged SpAdd: 1 when every partition fits a tile, else enough
+// kS4Tile - (k - 1) query-wide chunks for the largest partition (work <= max_work).
+int64_t staged_chunks(int64_t max_work, int32_t k) {
+  if (max_work <= kS4Tile) return 1;
+  const int64_t tq = kS4Tile - (k - 1);
+  return (max_work + tq - 1) / tq;
+}
+
+struct StagedWs {   // carving of the staged workspace for nchunk chunks
+  int64_t* cnt; unsigned long long* blk; int64_t* prov; int64_t* rows; char* stage;
+};
+size_t staged_ws_layout(int64_t nchunk, char* ws, StagedWs* out) {
+  size_t o = 0;
+  auto take = [&](size_t bytes) { const size_t at = o; o += align_up(bytes); return at; };
+  const size_t c = take((size_t)(nchunk + 1) * 8), b = take((size_t)((nchunk >> kS4BlkShift) + 1) * 8),
+               pv = take((size_t)nchunk * 8), r = take((size_t)nchunk * 16);
+  if (out) {
+    out->cnt = reinterpret_cast<int64_t*>(ws + c);
+    out->blk = reinterpret_cast<unsigned long long*>(ws + b);
+    out->prov = reinterpret_cast<int64_t*>(ws + pv);
+    out->rows = reinterpret_cast<int64_t*>(ws + r);
+    out->stage = ws + o;
+  }
+  return o;
+}
+
 template <typename T>
 nacho_status run_spadd_staged(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
-                              int64_t* z_pos, int32_t* z_crd, T* z_val, char* ws, cudaStream_t st) {
+                              int64_t* z_pos, int32_t* z_crd, T* z_val, char* ws, int64_t chunks, cudaStream_t st) {
   const int64_t q = total_cost(ops, k);
-  const size_t words = align_up((size_t)(parts->P + 1) * 8);
-  const int64_t nblk = ((int64_t)parts->P >> kS4BlkShift) + 1;
-  int64_t* cnt = reinterpret_cast<int64_t*>(ws);
-  auto* blk = reinterpret_cast<unsigned long long*>(ws + words);
-  int32_t* t_crd = reinterpret_cast<int32_t*>(ws + 2 * words);
-  T* t_val = reinterpret_cast<T*>(reinterpret_cast<char*>(t_crd) + align_up((size_t)q * 4));
-  if (cudaMemsetAsync(blk, 0, sizeof(unsigned long long) * nblk, st) != cudaSuccess)
+  const int64_t nchunk = (int64_t)parts->P * chunks;
+  StagedWs w;
+  staged_ws_layout(nchunk, ws, &w);
+  int32_t* t_crd = reinterpret_cast<int32_t*>(w.stage);
+  T* t_val = reinterpret_cast<T*>(w.stage + align_up((size_t)q * 4));
+  if (cudaMemsetAsync(w.blk, 0, sizeof(unsigned long long) * ((nchunk >> kS4BlkShift) + 1), st) != cudaSuccess)
     return fail(NACHO_ERR_CUDA, "memset block sums");
-  Spadd4Args<T> a{make_ops(ops, k), parts_arg(parts), cnt, part_off, nullptr, nullptr, z_pos, t_crd, t_val, blk};
-  NACHO_TRY((launch_spadd4<T, kS4Stage>(a, st)));
-  Spadd4Args<T> c{make_ops(ops, k), parts_arg(parts), cnt, part_off, nullptr, nullptr, z_pos, z_crd, z_val, blk};
-  s4_place_kernel<T><<<(unsigned)parts->P, kS4Threads, 0, st>>>(c, t_crd, t_val);
+  Spadd4Args<T> a{make_ops(ops, k), parts_arg(parts), w.cnt, part_off, nullptr, nullptr, z_pos, t_crd, t_val, w.blk,
+                  (int32_t)chunks, w.prov, w.rows};
+  NACHO_TRY((launch_spadd4<T, kS4Stage>(a, st, nchunk)));
+  Spadd4Args<T> c = a;
+  c.z_crd = z_crd;
+  c.z_val = z_val;
+  s4_place_kernel<T><<<(unsigned)nchunk, kS4Threads, 0, st>>>(c, t_crd, t_val);
   return launched("s4_place_kernel");
 }
 
@@ -531,7 +560,9 @@ size_t nacho_spadd_k_staged_workspace_size(const nacho_matrix* ops, int32_t k, i
   if (!ops || k < 1) return 0;
   const int64_t q = total_cost(ops, k);
   const size_t vs = ops[0].dtype == NACHO_F64 ? 8 : 4;
-  return 2 * align_up((size_t)((P > 0 ? P : 1) + 1) * 8) + align_up((size_t)q * 4) + align_up((size_t)q * vs);
+  const int64_t Pe = P > 0 ? P : 1;
+  const int64_t nchunk = Pe * staged_chunks((q + Pe - 1) / Pe + (k - 1), k);   // partitions of nacho_partition
+  return staged_ws_layout(nchunk, nullptr, nullptr) + align_up((size_t)q * 4) + align_up((size_t)q * vs);
 }
 
 /* Single read of the operands, no look-back: staged union + scan + placement (spadd4.cuh). */
@@ -544,15 +575,17 @@ nacho_status nacho_spadd_k_staged(const nacho_matrix* ops, int32_t k, const nach
   if (!z_pos || !part_off) return fail(NACHO_ERR_INVALID_ARG, "null z_pos / part_off");
   if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (!fits_sa_tile(ops, k, parts, st))
-    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kS4Tile);
-  const size_t need = nacho_spadd_k_staged_workspace_size(ops, k, parts->P);
+  const int64_t chunks = staged_chunks(max_part_work(ops, k, parts_arg(parts), kS4Tile, st), k);
+  const int64_t q = total_cost(ops, k);
+  const size_t vs = ops[0].dtype == NACHO_F64 ? 8 : 4;
+  const size_t need = staged_ws_layout((int64_t)parts->P * chunks, nullptr, nullptr) + align_up((size_t)q * 4) +
+                      align_up((size_t)q * vs);
   if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   if (ops[0].dtype == NACHO_F64)
     return run_spadd_staged<double>(ops, k, parts, part_off, z_pos, z_crd, static_cast<double*>(z_val),
-                                    static_cast<char*>(ws), st);
+                                    static_cast<char*>(ws), chunks, st);
   return run_spadd_staged<float>(ops, k, parts, part_off, z_pos, z_crd, static_cast<float*>(z_val),
-                                 static_cast<char*>(ws), st);
+                                 static_cast<char*>(ws), chunks, st);
 }
 
 // Carries of an SpMM over P partitions made by nacho_partition: one per tile-sized chunk.

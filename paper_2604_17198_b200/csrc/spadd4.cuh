@@ -74,7 +74,10 @@ struct Spadd4Args {
   int64_t* z_pos;
   int32_t* z_crd;
   T* z_val;
-  unsigned long long* blk_cnt;    // kS4Stage: union sizes summed per block of 2^kS4BlkShift partitions
+  unsigned long long* blk_cnt;    // kS4Stage: union sizes summed per block of 2^kS4BlkShift chunks
+  int32_t chunks;                 // kS4Stage: CTAs (chunks) per partition; 1 unless partitions exceed a tile
+  int64_t* ch_prov;               // kS4Stage: per chunk, provisional offset sum_o b.pos[o]
+  int64_t* ch_row;                // kS4Stage: per chunk, [2*c] first row, [2*c+1] end row
 };
 
 // Padded slot of element i of a thread-blocked stage buffer (conflict-free blocked accesses).
@@ -93,6 +96,8 @@ struct S4Shared {
   const int64_t* posp[NACHO_MAX_K];       // pos_o + row0 + 1
   int64_t p;
   int64_t bcast;
+  int64_t cpos[2][NACHO_MAX_K];           // chunked staged mode: the chunk's start / end positions
+  int64_t crow[2];
   int32_t ired[kS4Threads / 32];
   int32_t fred_f[kS4Threads / 32], fred_v[kS4Threads / 32];
   int32_t cmn[kS4Threads / 32], cmx[kS4Threads / 32];
@@ -583,7 +588,13 @@ __device__ __forceinline__ void s4_dense(const Spadd4Args<T>& a, SH& sh, int64_t
 #pragma unroll
     for (int o = 0; o < KM; ++o) if (o < k) off += sh.b0pos[o];
     pos_off = 0;
-    if (tid == 0) { a.part_cnt[p] = nu; atomicAdd(a.blk_cnt + (p >> kS4BlkShift), (unsigned long long)nu); }
+    if (tid == 0) {
+      a.part_cnt[p] = nu;
+      atomicAdd(a.blk_cnt + (p >> kS4BlkShift), (unsigned long long)nu);
+      a.ch_prov[p] = off;
+      a.ch_row[2 * p] = row0;
+      a.ch_row[2 * p + 1] = row1;
+    }
   } else {
     if (w == 0) {
       const int64_t ex = s4_lookback(a.lb_state, p, nu);
@@ -694,6 +705,9 @@ __device__ __forceinline__ void s4_body(const Spadd4Args<T>& a, SH& sh, int64_t 
     if (MODE == kS4Stage && tid == 0) {
       a.part_cnt[p] = nu;
       atomicAdd(a.blk_cnt + (p >> kS4BlkShift), (unsigned long long)nu);
+      a.ch_prov[p] = out.off;
+      a.ch_row[2 * p] = row0;
+      a.ch_row[2 * p + 1] = row1;
     }
     S4PH(4);
     return;
@@ -774,14 +788,45 @@ __global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 1280 / kS4Thr
   } else {
     p = blockIdx.x;
   }
+  // ---- staged mode, partitions larger than a tile: CTA p is chunk c of partition pp, the part of it
+  //      between the queries C(b_pp) + c Tq and C(b_pp) + (c+1) Tq -- two more FindPartition (Alg. 1)
+  //      searches, whose cuts coincide with the global partition's for those queries, so chunks tile
+  //      the partition and every coordinate lies in one chunk (work <= Tq + k - 1 = kS4Tile)
+  const bool chunked = MODE == kS4Stage && a.chunks > 1;
+  if (chunked) {
+    if (w < 2) {
+      const int64_t pp = p / a.chunks, c = p - pp * a.chunks;
+      int64_t C0 = 0, C1 = 0;
+      for (int o = 0; o < k; ++o) { C0 += ldg(a.parts.pos + pp * k + o); C1 += ldg(a.parts.pos + (pp + 1) * k + o); }
+      const int64_t Tq = kS4Tile - (k - 1);
+      const int64_t Q = C0 + (c + w) * Tq;
+      int64_t row, pos[KM];
+      if ((w == 0 && c == 0) || Q >= C1) {   // the partition's own boundary
+        const int64_t q = (w == 0 && c == 0) ? pp : pp + 1;
+        row = ldg(a.parts.row + q);
+#pragma unroll
+        for (int o = 0; o < KM; ++o) pos[o] = o < k ? ldg(a.parts.pos + q * k + o) : 0;
+      } else {
+        const Boundary b = warp_find_boundary<KM>(a.ops, Q, ldg(a.parts.row_pos + pp), ldg(a.parts.row_pos + pp + 1));
+        row = b.row;
+#pragma unroll
+        for (int o = 0; o < KM; ++o) pos[o] = b.pos[o];
+      }
+      if (lane == 0) sh.crow[w] = row;
+#pragma unroll
+      for (int o = 0; o < KM; ++o) if (lane == o && o < k) sh.cpos[w][o] = pos[o];
+    }
+    __syncthreads();
+  }
   // ---- boundaries and operand ranges (warp 0: lane o < k holds operand o; sizes scanned by shuffles)
-  const int64_t row0 = ldg(a.parts.row + p), row1 = ldg(a.parts.row + p + 1);
+  const int64_t row0 = chunked ? sh.crow[0] : ldg(a.parts.row + p);
+  const int64_t row1 = chunked ? sh.crow[1] : ldg(a.parts.row + p + 1);
   if (w == 0) {
     int64_t b0 = 0;
     int sz = 0;
     if (lane < k) {
-      b0 = ldg(a.parts.pos + p * k + lane);
-      sz = (int)(ldg(a.parts.pos + (p + 1) * k + lane) - b0);
+      b0 = chunked ? sh.cpos[0][lane] : ldg(a.parts.pos + p * k + lane);
+      sz = (int)((chunked ? sh.cpos[1][lane] : ldg(a.parts.pos + (p + 1) * k + lane)) - b0);
     }
     int inc = sz;
 #pragma unroll
@@ -942,13 +987,12 @@ __global__ void __launch_bounds__(kS4Threads) s4_place_kernel(const __grid_const
   for (int ww = 0; ww < kS4Threads / 32; ++ww) tot += s_red[ww];
   const int64_t off = (int64_t)tot;
   const int64_t nu = ldg(a.part_cnt + p);
-  if (tid == 0) {
-    a.part_off[p] = off;
-    if (p == a.parts.P - 1) a.part_off[a.parts.P] = off + nu;
+  if (tid == 0) {   // p is a chunk; partition pp's offset is that of its first chunk
+    const int64_t pp = p / a.chunks;
+    if (p == pp * a.chunks) a.part_off[pp] = off;
+    if (p == (int64_t)a.parts.P * a.chunks - 1) a.part_off[a.parts.P] = off + nu;
   }
-  const int k = a.ops.k;
-  int64_t prov = 0;
-  for (int o = 0; o < k; ++o) prov += ldg(a.parts.pos + p * k + o);
+  const int64_t prov = ldg(a.ch_prov + p);
   constexpr int U = 4;   // loads in flight per thread
   for (int64_t jb = 0; jb < nu; jb += U * kS4Threads) {
     int32_t c[U];
@@ -964,7 +1008,7 @@ __global__ void __launch_bounds__(kS4Threads) s4_place_kernel(const __grid_const
       if (j < nu) { a.z_crd[off + j] = c[u]; a.z_val[off + j] = vv[u]; }
     }
   }
-  const int64_t r0 = ldg(a.parts.row + p), r1 = ldg(a.parts.row + p + 1);
+  const int64_t r0 = ldg(a.ch_row + 2 * p), r1 = ldg(a.ch_row + 2 * p + 1);
   for (int64_t r = r0 + tid; r < r1; r += kS4Threads) a.z_pos[r + 1] += off;
 }
 

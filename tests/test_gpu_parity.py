@@ -170,6 +170,15 @@ def _spadd_check(ops, P=None):
     assert np.array_equal(z_pos.cpu().numpy(), rp), "Z.pos"
     assert np.array_equal(z_crd.cpu().numpy(), rc), "Z.crd"
     assert np.array_equal(z_val.cpu().numpy().view(np.uint8), rv.view(np.uint8)), "Z.val bits"
+    # staged single-read variant: any P (partitions larger than a tile run as Alg.-1-cut chunks)
+    so = torch.full((parts.P + 1,), -1, dtype=torch.int64, device=DEV)
+    sz_pos, sz_crd, sz_val = N.spadd_k_staged(dops, parts, part_off=so)
+    n = int(sz_pos[-1].item())
+    assert n == len(rc)
+    assert np.array_equal(so.cpu().numpy(), np.concatenate([[0], np.cumsum(cnt)])), "staged part_off"
+    assert np.array_equal(sz_pos.cpu().numpy(), rp), "staged Z.pos"
+    assert np.array_equal(sz_crd[:n].cpu().numpy(), rc), "staged Z.crd"
+    assert np.array_equal(sz_val[:n].cpu().numpy().view(np.uint8), rv.view(np.uint8)), "staged Z.val bits"
     # single-pass (look-back) variant, when the partitions fit its tile
     qstar = sum(A.nnz for A in ops)
     if -(-qstar // parts.P) + len(ops) - 1 <= 2048:
@@ -181,15 +190,7 @@ def _spadd_check(ops, P=None):
         assert np.array_equal(fz_pos.cpu().numpy(), rp), "fused Z.pos"
         assert np.array_equal(fz_crd[:n].cpu().numpy(), rc), "fused Z.crd"
         assert np.array_equal(fz_val[:n].cpu().numpy().view(np.uint8), rv.view(np.uint8)), "fused Z.val bits"
-        # staged variant (single read, no look-back: staging buffer + scan + placement)
-        so = torch.full((parts.P + 1,), -1, dtype=torch.int64, device=DEV)
-        sz_pos, sz_crd, sz_val = N.spadd_k_staged(dops, parts, part_off=so)
-        n = int(sz_pos[-1].item())
-        assert n == len(rc)
-        assert np.array_equal(so.cpu().numpy(), np.concatenate([[0], np.cumsum(cnt)])), "staged part_off"
-        assert np.array_equal(sz_pos.cpu().numpy(), rp), "staged Z.pos"
-        assert np.array_equal(sz_crd[:n].cpu().numpy(), rc), "staged Z.crd"
-        assert np.array_equal(sz_val[:n].cpu().numpy().view(np.uint8), rv.view(np.uint8)), "staged Z.val bits"
+
 
 
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 8])
