@@ -157,7 +157,7 @@ nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts
  *   always enough).
  *   ws  >= nacho_spadd_k_staged_workspace_size(ops, k, P) bytes: per-chunk counts, offsets and rows +
  *   Q* staged (col, value) pairs (sized for partitions from nacho_partition; a record whose max_work
- *   exceeds ceil(Q*/P) + k - 1 may need more: WORKSPACE).  Errors as nacho_spadd_k. */
+ *   exceeds ceil(Q* / P) + k - 1 may need more: WORKSPACE).  Errors as nacho_spadd_k. */
 size_t nacho_spadd_k_staged_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P);
 nacho_status nacho_spadd_k_staged(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
                                   int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes,
