@@ -220,9 +220,9 @@ nacho_status launch_spadd(const SpaddArgs<T>& a, cudaStream_t st) {
   return launched(FILL ? "spadd_fill_kernel" : "spadd_count_kernel");
 }
 
-template <typename T, int MODE, int KM>
+template <typename T, int MODE, int KM, bool CHK>
 nacho_status launch_spadd4_k(const Spadd4Args<T>& a, cudaStream_t st, int64_t grid) {
-  auto kern = spadd4_kernel<T, MODE, KM>;
+  auto kern = spadd4_kernel<T, MODE, KM, CHK>;
   const size_t smem = sizeof(S4Shared<T, s4_small(MODE, KM)>);
   static bool configured = false;
   if (!configured) {
@@ -239,11 +239,19 @@ nacho_status launch_spadd4_k(const Spadd4Args<T>& a, cudaStream_t st, int64_t gr
 template <typename T, int MODE>
 nacho_status launch_spadd4(const Spadd4Args<T>& a, cudaStream_t st, int64_t grid = -1) {
   if (grid < 0) grid = a.parts.P;
+  if (MODE == kS4Stage && a.chunks > 1) {
+    switch (a.ops.k) {
+      case 1: return launch_spadd4_k<T, MODE, 1, true>(a, st, grid);
+      case 2: return launch_spadd4_k<T, MODE, 2, true>(a, st, grid);
+      case 3: return launch_spadd4_k<T, MODE, 3, true>(a, st, grid);
+      default: return launch_spadd4_k<T, MODE, NACHO_MAX_K, true>(a, st, grid);
+    }
+  }
   switch (a.ops.k) {
-    case 1: return launch_spadd4_k<T, MODE, 1>(a, st, grid);
-    case 2: return launch_spadd4_k<T, MODE, 2>(a, st, grid);
-    case 3: return launch_spadd4_k<T, MODE, 3>(a, st, grid);
-    default: return launch_spadd4_k<T, MODE, NACHO_MAX_K>(a, st, grid);
+    case 1: return launch_spadd4_k<T, MODE, 1, false>(a, st, grid);
+    case 2: return launch_spadd4_k<T, MODE, 2, false>(a, st, grid);
+    case 3: return launch_spadd4_k<T, MODE, 3, false>(a, st, grid);
+    default: return launch_spadd4_k<T, MODE, NACHO_MAX_K, false>(a, st, grid);
   }
 }
 

@@ -771,7 +771,7 @@ __device__ __noinline__ void s4_body64(const Spadd4Args<T>& a, SH& sh, int64_t p
   s4_body<T, uint64_t, MODE, KM, SH>(a, sh, p, n, row0, row1, 32, cmin, s4t);
 }
 
-template <typename T, int MODE, int KM>
+template <typename T, int MODE, int KM, bool CHK>   // CHK: staged mode, partitions larger than a tile
 __global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 1280 / kS4Threads : NACHO_S4_MINB) spadd4_kernel(const __grid_constant__ Spadd4Args<T> a) {
   constexpr bool VALS = MODE != kS4Count;
   extern __shared__ __align__(16) unsigned char s4raw[];
@@ -792,8 +792,8 @@ __global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 1280 / kS4Thr
   //      between the queries C(b_pp) + c Tq and C(b_pp) + (c+1) Tq -- two more FindPartition (Alg. 1)
   //      searches, whose cuts coincide with the global partition's for those queries, so chunks tile
   //      the partition and every coordinate lies in one chunk (work <= Tq + k - 1 = kS4Tile)
-  const bool chunked = MODE == kS4Stage && a.chunks > 1;
-  if (chunked) {
+  constexpr bool chunked = MODE == kS4Stage && CHK;
+  if constexpr (chunked) {
     if (w < 2) {
       const int64_t pp = p / a.chunks, c = p - pp * a.chunks;
       int64_t C0 = 0, C1 = 0;
