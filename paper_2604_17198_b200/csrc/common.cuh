@@ -131,42 +131,48 @@ __device__ __forceinline__ int lanes_less(V v, V x, int n) {
 // exactly with lane shuffles.
 // KM: compile-time bound on k (register arrays sized KM).  Column values are int32 (crd < ncols <=
 // INT32_MAX), so INT32_MAX is a safe "past the window" value.
-template <int KM>
-__device__ __forceinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&lo)[KM], int64_t (&hi)[KM], int64_t R,
-                                              Boundary& b) {
+// I: window index type.  The windows are offsets from cp[o] (the row segment's first entry); the
+// caller takes I = int32_t when the segments' total length is below 2^26 (every product and rank
+// below fits 32 bits: half the instructions of the 64-bit form), int64_t otherwise.
+template <int KM, typename I>
+__device__ __forceinline__ void warp_kway_select_t(const int32_t* const (&cp)[KM], int k, I (&lo)[KM], I (&hi)[KM], I R,
+                                                int32_t& col, I (&pos)[KM]) {
   const int lane = threadIdx.x & 31;
   constexpr int32_t INF = INT32_MAX;
   for (;;) {
     int m = 0;
-    int64_t lmax = -1;
+    I lmax = -1;
 #pragma unroll
     for (int o = 0; o < KM; ++o)
       if (o < k && hi[o] - lo[o] > lmax) { lmax = hi[o] - lo[o]; m = o; }
     if (lmax <= 32) break;
-    int64_t sp[KM];
+    I sp[KM];
     int32_t u[KM];
 #pragma unroll
     for (int o = 0; o < KM; ++o) {
       if (o < k) {
-        const int64_t len = hi[o] - lo[o];
-        if (len > 0) { sp[o] = lo[o] + ((int64_t)(lane + 1) * len) / 33; u[o] = (int32_t)ldg(a.op[o].crd + sp[o]); }
-        else { sp[o] = lo[o]; u[o] = INF; }
+        const I len = hi[o] - lo[o];
+        if (len > 0) {
+          if constexpr (sizeof(I) == 4) sp[o] = lo[o] + (I)(((uint32_t)(lane + 1) * (uint32_t)len) / 33u);
+          else sp[o] = lo[o] + ((int64_t)(lane + 1) * len) / 33;
+          u[o] = (int32_t)ldg(cp[o] + sp[o]);
+        } else { sp[o] = lo[o]; u[o] = INF; }
       }
     }
     int32_t cand = 0;
-    int64_t own = 0, spm = 0;
+    I own = 0, spm = 0;
 #pragma unroll
     for (int o = 0; o < KM; ++o)
       if (o == m) { cand = u[o]; spm = sp[o]; own = sp[o] - lo[o]; }
-    int64_t L = own, U = own;
-    int64_t Lo[KM], Uo[KM];
+    I L = own, U = own;
+    I Lo[KM], Uo[KM];
 #pragma unroll
     for (int o = 0; o < KM; ++o) {
       if (o < k) {
-        const int64_t len = hi[o] - lo[o];
+        const I len = hi[o] - lo[o];
         const int j = lanes_less(u[o], cand, len > 0 ? 32 : 0);
-        const int64_t sjm = __shfl_sync(kFull, sp[o], j > 0 ? j - 1 : 0);
-        const int64_t sj = __shfl_sync(kFull, sp[o], j < 32 ? j : 31);
+        const I sjm = __shfl_sync(kFull, sp[o], j > 0 ? j - 1 : 0);
+        const I sj = __shfl_sync(kFull, sp[o], j < 32 ? j : 31);
         Lo[o] = j > 0 ? sjm - lo[o] + 1 : 0;
         Uo[o] = j < 32 ? sj - lo[o] : len;
         if (o != m) { L += Lo[o]; U += Uo[o]; }
@@ -176,14 +182,14 @@ __device__ __forceinline__ void warp_kway_select(const OpsArg& a, int k, int64_t
     const unsigned above = __ballot_sync(kFull, L > R);    // candidates >  v*
     const int ia = below ? 31 - __clz(below) : -1;
     const int ib = above ? __ffs(above) - 1 : 32;
-    int64_t drop = 0;
+    I drop = 0;
 #pragma unroll
     for (int o = 0; o < KM; ++o) {
       if (o < k) {
-        const int64_t la = __shfl_sync(kFull, o == m ? spm - lo[o] : Lo[o], ia >= 0 ? ia : 0);
-        const int64_t ub = __shfl_sync(kFull, o == m ? spm - lo[o] : Uo[o], ib < 32 ? ib : 0);
-        const int64_t nlo = ia >= 0 ? lo[o] + la : lo[o];
-        const int64_t nhi = ib < 32 ? lo[o] + ub : hi[o];
+        const I la = __shfl_sync(kFull, o == m ? spm - lo[o] : Lo[o], ia >= 0 ? ia : 0);
+        const I ub = __shfl_sync(kFull, o == m ? spm - lo[o] : Uo[o], ib < 32 ? ib : 0);
+        const I nlo = ia >= 0 ? lo[o] + la : lo[o];
+        const I nhi = ib < 32 ? lo[o] + ub : hi[o];
         drop += nlo - lo[o];
         lo[o] = nlo;
         hi[o] = nhi;
@@ -195,7 +201,7 @@ __device__ __forceinline__ void warp_kway_select(const OpsArg& a, int k, int64_t
   int32_t e[KM];
 #pragma unroll
   for (int o = 0; o < KM; ++o)
-    if (o < k) e[o] = (lane < hi[o] - lo[o]) ? (int32_t)ldg(a.op[o].crd + lo[o] + lane) : INF;
+    if (o < k) e[o] = (lane < hi[o] - lo[o]) ? (int32_t)ldg(cp[o] + lo[o] + lane) : INF;
   // rank of lane l's entry of window o in the multiset union ordered by (column, operand):
   // entries of lower operands with a column <= it, of higher operands with a column < it, and the l
   // entries before it in its own window -- unique ranks, so exactly one entry has rank R
@@ -204,7 +210,7 @@ __device__ __forceinline__ void warp_kway_select(const OpsArg& a, int k, int64_t
   for (int o = 0; o < KM; ++o) {
     if (o < k) {
       const int32_t x = e[o];
-      int64_t rank = lane;
+      int rank = lane;
 #pragma unroll
       for (int o2 = 0; o2 < KM; ++o2) {
         if (o2 < k && o2 != o) {
@@ -212,14 +218,52 @@ __device__ __forceinline__ void warp_kway_select(const OpsArg& a, int k, int64_t
           rank += lanes_less(e[o2], (o2 < o && x != INF) ? x + 1 : x, n2);
         }
       }
-      const unsigned hm = __ballot_sync(kFull, x != INF && rank == R);
+      const unsigned hm = __ballot_sync(kFull, x != INF && (I)rank == R);
       if (hm) vstar = __shfl_sync(kFull, x, __ffs(hm) - 1);
     }
   }
-  b.col = vstar;
+  col = vstar;
 #pragma unroll
   for (int o = 0; o < KM; ++o)
-    if (o < k) b.pos[o] = lo[o] + __popc(__ballot_sync(kFull, e[o] < vstar));
+    if (o < k) pos[o] = lo[o] + __popc(__ballot_sync(kFull, e[o] < vstar));
+}
+
+template <int KM>
+__device__ __noinline__ void warp_kway_select64(const OpsArg& a, int k, int64_t (&lo)[KM], int64_t (&hi)[KM], int64_t R,
+                                               Boundary& b) {
+  const int32_t* cp[KM];
+  int64_t l64[KM], h64[KM], p64[KM];
+#pragma unroll
+  for (int o = 0; o < KM; ++o)
+    if (o < k) { cp[o] = a.op[o].crd + lo[o]; l64[o] = 0; h64[o] = hi[o] - lo[o]; }
+  warp_kway_select_t<KM, int64_t>(cp, k, l64, h64, R, b.col, p64);
+#pragma unroll
+  for (int o = 0; o < KM; ++o)
+    if (o < k) b.pos[o] = lo[o] + p64[o];
+}
+
+// The (R+1)-th smallest column of the multiset union of the row segments crd_o[lo_o, hi_o) (absolute
+// positions) and its lower-bound position in every operand: the inner level of FindPartition.
+template <int KM>
+__device__ __forceinline__ void warp_kway_select(const OpsArg& a, int k, int64_t (&lo)[KM], int64_t (&hi)[KM], int64_t R,
+                                              Boundary& b) {
+  const int32_t* cp[KM];
+  int64_t tot = 0;
+#pragma unroll
+  for (int o = 0; o < KM; ++o)
+    if (o < k) { cp[o] = a.op[o].crd + lo[o]; tot += hi[o] - lo[o]; }
+  if (tot < ((int64_t)1 << 26)) {
+    int32_t l32[KM], h32[KM], p32[KM];
+#pragma unroll
+    for (int o = 0; o < KM; ++o)
+      if (o < k) { l32[o] = 0; h32[o] = (int32_t)(hi[o] - lo[o]); }
+    warp_kway_select_t<KM, int32_t>(cp, k, l32, h32, (int32_t)R, b.col, p32);
+#pragma unroll
+    for (int o = 0; o < KM; ++o)
+      if (o < k) b.pos[o] = lo[o] + p32[o];
+  } else {
+    warp_kway_select64<KM>(a, k, lo, hi, R, b);   // segments of 2^26 entries or more: out of line
+  }
 }
 
 // FindPartition (Alg. 1) for query Q, executed by one full warp; every lane returns

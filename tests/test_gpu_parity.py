@@ -67,6 +67,20 @@ def test_partition_configs(name, scale, P):
     _parts_equal(gp, O.partition_rank([A.numpy() for A in wl.ops], P))
 
 
+def test_partition_long_row_segments():
+    """One row whose segments total >= 2^26 entries: the k-way select's 64-bit window path (the
+    32-bit path serves shorter segments); boundaries bit-exact against the oracle."""
+    rng = np.random.default_rng(2026)
+    n = 3 << 23                                        # 3 * 2^23 per operand, 3 operands: 1.125 * 2^26
+    ops = []
+    for o in range(3):
+        crd = np.cumsum(rng.integers(1, 40, n)).astype(np.int64)
+        pos = np.array([0, 0, n, n], np.int64)         # rows 0 and 2 empty, row 1 holds everything
+        ops.append(W.SparseMatrix(W.CSR, 3, 40 * n, pos, crd.astype(np.int32), np.ones(n, np.float32)))
+    for P in (1, 5, 64):
+        _parts_equal(N.partition([_dev(A) for A in ops], P), O.partition_rank(ops, P))
+
+
 def test_device_generator_matches_numpy_recipe():
     for name, scale in [("c1", 1.0), ("c2", 0.01), ("c3", 0.002), ("c4", 1e-4), ("c5", 2e-5)]:
         d = W.build(name, scale, device="cuda")
