@@ -24,5 +24,13 @@ else
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"spmv3_kernel" -s 1 -c 1 \
       -o gpurun_out/full_c3 -f python profiles/run_once.py c3 --steps 2 > gpurun_out/ncu_full_c3.log 2>&1
 fi
+# summaries on the box; the reports themselves only with KEEP_REPS=1 (gpurun returns <= 64 MiB)
+for r in gpurun_out/full_*.ncu-rep; do
+  [ -f "$r" ] || continue
+  b=$(basename "$r" .ncu-rep)
+  python profiles/ncu_summary.py "$r" > "gpurun_out/ncu_${b}.txt" 2>&1
+  python profiles/src_hot.py "$r" 60 > "gpurun_out/src_${b}.txt" 2>&1
+  [ "${KEEP_REPS:-0}" = "1" ] || rm -f "$r"
+done
 nvidia-smi --query-gpu=name,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt
 lscpu | grep -E "Model name|^CPU\(s\)" >> gpurun_out/gpu.txt
