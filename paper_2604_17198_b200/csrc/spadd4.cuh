@@ -967,17 +967,31 @@ __global__ void __launch_bounds__(kS4Threads, s4_small(MODE, KM) ? 1280 / kS4Thr
 // here from the per-256-partition block sums the stage kernel accumulated plus the sizes of p's
 // predecessors inside its block (no separate scan kernel).  One CTA per partition.
 template <typename T>
-__global__ void __launch_bounds__(kS4Threads) s4_place_kernel(const __grid_constant__ Spadd4Args<T> a,
+__global__ void __launch_bounds__(kS4Threads, 6) s4_place_kernel(const __grid_constant__ Spadd4Args<T> a,
                                                                const int32_t* __restrict__ t_crd,
                                                                const T* __restrict__ t_val) {
   __shared__ unsigned long long s_red[kS4Threads / 32];
   const int64_t p = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // every load that does not depend on the offset is issued before the offset's reduction, so a
+  // CTA waits on about two DRAM round trips instead of four
+  const int64_t nu = ldg(a.part_cnt + p), prov = ldg(a.ch_prov + p);
+  const int64_t r0 = ldg(a.ch_row + 2 * p), r1 = ldg(a.ch_row + 2 * p + 1);
   const int64_t b = p >> kS4BlkShift;
   unsigned long long v = 0;
   for (int64_t i = tid; i < b; i += kS4Threads) v += a.blk_cnt[i];
   const int64_t q = (b << kS4BlkShift) + tid;
   if (q < p) v += (unsigned long long)ldg(a.part_cnt + q);
+  constexpr int U = kS4Tile / kS4Threads;   // a chunk's union fits one round (nu <= kS4Tile)
+  int32_t c[U];
+  T vv[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = u * kS4Threads + tid;
+    if (j < nu) { c[u] = __ldcs(t_crd + prov + j); vv[u] = __ldcs(t_val + prov + j); }
+  }
+  const int64_t rr = r0 + tid;
+  const int64_t zp0 = rr < r1 ? a.z_pos[rr + 1] : 0;
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
   if (lane == 0) s_red[w] = v;
@@ -986,30 +1000,22 @@ __global__ void __launch_bounds__(kS4Threads) s4_place_kernel(const __grid_const
 #pragma unroll
   for (int ww = 0; ww < kS4Threads / 32; ++ww) tot += s_red[ww];
   const int64_t off = (int64_t)tot;
-  const int64_t nu = ldg(a.part_cnt + p);
   if (tid == 0) {   // p is a chunk; partition pp's offset is that of its first chunk
     const int64_t pp = p / a.chunks;
     if (p == pp * a.chunks) a.part_off[pp] = off;
     if (p == (int64_t)a.parts.P * a.chunks - 1) a.part_off[a.parts.P] = off + nu;
   }
-  const int64_t prov = ldg(a.ch_prov + p);
-  constexpr int U = 4;   // loads in flight per thread
-  for (int64_t jb = 0; jb < nu; jb += U * kS4Threads) {
-    int32_t c[U];
-    T vv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = jb + u * kS4Threads + tid;
-      if (j < nu) { c[u] = __ldcs(t_crd + prov + j); vv[u] = __ldcs(t_val + prov + j); }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = jb + u * kS4Threads + tid;
-      if (j < nu) { a.z_crd[off + j] = c[u]; a.z_val[off + j] = vv[u]; }
-    }
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = u * kS4Threads + tid;
+    if (j < nu) { a.z_crd[off + j] = c[u]; a.z_val[off + j] = vv[u]; }
   }
-  const int64_t r0 = ldg(a.ch_row + 2 * p), r1 = ldg(a.ch_row + 2 * p + 1);
-  for (int64_t r = r0 + tid; r < r1; r += kS4Threads) a.z_pos[r + 1] += off;
+  for (int64_t j = U * kS4Threads + tid; j < nu; j += kS4Threads) {   // not reached (nu <= kS4Tile)
+    a.z_crd[off + j] = t_crd[prov + j];
+    a.z_val[off + j] = t_val[prov + j];
+  }
+  if (rr < r1) a.z_pos[rr + 1] = zp0 + off;
+  for (int64_t r = rr + kS4Threads; r < r1; r += kS4Threads) a.z_pos[r + 1] += off;
 }
 
 }  // namespace nacho
