@@ -44,7 +44,9 @@ struct PartsArg {
 // Q_p = floor(p * Q* / P) without 128-bit arithmetic: (Q*/P)*p + ((Q*%P)*p)/P is exact because
 // (Q*%P)*p < P*P <= 2^62 (reading R4).
 __host__ __device__ __forceinline__ int64_t query_of(int64_t qstar, int64_t P, int64_t p) {
-  return (qstar / P) * p + ((qstar % P) * p) / P;
+  const int64_t r = qstar % P;   // (r p) / P: 32-bit when r p < 2^32 (P < 2^16), the usual case
+  const int64_t t = (P < 65536) ? (int64_t)((uint32_t)(r * p) / (uint32_t)P) : (r * p) / P;
+  return (qstar / P) * p + t;
 }
 
 template <typename T>
@@ -57,6 +59,24 @@ __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
 template <typename Pred>
 __device__ __forceinline__ int64_t warp_highest_true(int64_t lo, int64_t hi, Pred pred) {
   const int lane = threadIdx.x & 31;
+  if (hi < ((int64_t)1 << 26)) {   // 32-bit index arithmetic ((lane + 1) * span < 2^31)
+    int32_t l = (int32_t)lo, h = (int32_t)hi;
+    while (h > l) {
+      const int32_t span = h - l;
+      int32_t x = (span <= 32) ? l + lane + 1 : l + (((lane + 1) * span + 31) >> 5);
+      if (x > h) x = h;
+      const bool ok = pred((int64_t)x);
+      const unsigned m = __ballot_sync(kFull, ok);
+      const int32_t x0 = __shfl_sync(kFull, x, 0);
+      if (m == 0) { h = x0 - 1; continue; }
+      const int j = 31 - __clz(m);
+      const int32_t xj = __shfl_sync(kFull, x, j);
+      const int32_t xn = __shfl_sync(kFull, x, j < 31 ? j + 1 : 31);
+      l = xj;
+      if (j < 31 && xn > xj) h = xn - 1;
+    }
+    return l;
+  }
   while (hi > lo) {
     const int64_t span = hi - lo;
     int64_t x = (span <= 32) ? lo + lane + 1 : lo + (((int64_t)(lane + 1) * span + 31) >> 5);
