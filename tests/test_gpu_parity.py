@@ -81,6 +81,33 @@ def test_partition_long_row_segments():
         _parts_equal(N.partition([_dev(A) for A in ops], P), O.partition_rank(ops, P))
 
 
+def test_partition_many_rows():
+    """More than 2^26 rows: the outer search's 64-bit index path (32-bit below 2^26 rows), k = 1 and
+    k = 2, boundaries bit-exact against the oracle."""
+    rng = np.random.default_rng(2027)
+    M, Nc = (1 << 26) + 1000, 5000
+    ops = []
+    for o in range(2):
+        rows = np.sort(rng.choice(M, size=6000, replace=False))
+        rows[-1] = M - 1                                  # reach the last rows
+        cnt = np.zeros(M + 1, np.int64)
+        per = rng.integers(1, 4, len(rows))
+        cnt[rows + 1] = per
+        pos = np.cumsum(cnt)
+        crd = np.concatenate([np.sort(rng.choice(Nc, size=c, replace=False)) for c in per]).astype(np.int32)
+        ops.append(W.SparseMatrix(W.CSR, M, Nc, pos, crd, np.ones(len(crd), np.float32)))
+    for k in (1, 2):
+        for P in (1, 7, 300):
+            _parts_equal(N.partition([_dev(A) for A in ops[:k]], P), O.partition_rank(ops[:k], P))
+    # SpMV over the same rows: few partitions, so chunks search their rows (64-bit outer indices)
+    A = ops[0]
+    x = rng.uniform(-1, 1, Nc).astype(np.float32)
+    dA = _dev(A)
+    for P in (1, 3):
+        y = N.spmv(dA, torch.from_numpy(x).to(DEV), N.partition([dA], P)).cpu().numpy()
+        _spmv_check(A, x, y, 1e-5)
+
+
 def test_device_generator_matches_numpy_recipe():
     for name, scale in [("c1", 1.0), ("c2", 0.01), ("c3", 0.002), ("c4", 1e-4), ("c5", 2e-5)]:
         d = W.build(name, scale, device="cuda")
