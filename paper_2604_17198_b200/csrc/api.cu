@@ -47,7 +47,10 @@ constexpr int kSpaddThreads = 256;
 constexpr int kSpaddTile = 2048;  // entries (summed over operands) per CTA chunk
 constexpr int kSpmmWarps = 8;
 constexpr int kSpmmWitems = 128;  // 1024 positions per CTA
-constexpr int kPartWarps = 4;
+#ifndef NACHO_PART_WARPS   // tuning override
+#define NACHO_PART_WARPS 4
+#endif
+constexpr int kPartWarps = NACHO_PART_WARPS;
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
