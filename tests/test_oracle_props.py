@@ -228,3 +228,102 @@ def test_spadd_against_dense(k):
             b = list(zip(parts.row.tolist(), parts.col.tolist()))
             bf = [sum(1 for c in keys if b[p] <= c < b[p + 1]) for p in range(P)]
             assert cnt.tolist() == bf
+
+
+# ---------------------------------------------------------------- fp64 branches and validation codes
+def _spread_values(rng, n):
+    """fp64 values over ~30 binades with random signs: the order of a three-term sum then changes the
+    rounded result for many entries, so a fold in any other order than the left fold fails the pin."""
+    return rng.uniform(1.0, 2.0, n) * np.exp2(rng.integers(-15, 15, n)) * rng.choice([-1.0, 1.0], n)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_spadd_f64_left_fold_against_dense(k):
+    """oracle_spadd_k's fp64 branch (R9 left fold in operand order) against a dense fp64 evaluation
+    ((0 + a_0) + a_1) + ... with absent terms +0 (x + 0 = x exactly for x != -0): bit-exact."""
+    rng = np.random.default_rng(40 + k)
+    order_matters = 0
+    for trial in range(15):
+        M, N = int(rng.integers(1, 30)), int(rng.integers(1, 30))
+        base = random_csr(rng, M, N, 0.35, dtype=np.float64)
+        ops = [base] + [random_csr(rng, M, N, 0.25, dtype=np.float64, base=base, share=0.6) for _ in range(k - 1)]
+        for A in ops:
+            A.val[:] = _spread_values(rng, A.nnz)
+        z_pos, z_crd, z_val = O.spadd_k(ops)
+        mask = np.zeros((M, N), bool)
+        dense = np.zeros((M, N), np.float64)
+        rdense = np.zeros((M, N), np.float64)
+        Ds = [W.to_dense(A) for A in ops]
+        for A, D in zip(ops, Ds):
+            mask |= D != 0
+            dense = dense + D                              # left fold in operand order
+        for D in reversed(Ds):
+            rdense = rdense + D                            # right-to-left fold, for discrimination only
+        rows, cols = np.nonzero(mask)
+        assert z_val.dtype == np.float64
+        assert z_pos.tolist() == np.concatenate([[0], np.cumsum(mask.sum(axis=1))]).tolist()
+        assert z_crd.tolist() == cols.tolist()
+        assert np.array_equal(z_val, dense[rows, cols])
+        order_matters += int((dense[rows, cols] != rdense[rows, cols]).sum())
+    if k >= 3:
+        assert order_matters > 0, "inputs do not discriminate the fold order"
+
+
+def test_spmm_f64_against_dense():
+    """oracle_spmm's fp64 branch: within 1e-12 of a dense fp64 product (relative to sum|a b|), which an
+    fp32 read of A or B (~1e-8) would fail; and exact on small integers (all partial sums < 2^53)."""
+    rng = np.random.default_rng(41)
+    for nb in (1, 7, 64):
+        A = random_csr(rng, 45, 37, 0.25, dtype=np.float64, dense_rows=[2])
+        A.val[:] = rng.uniform(0.5, 1.5, A.nnz) + rng.uniform(0, 1e-9, A.nnz)   # fp64-only digits
+        B = (rng.uniform(0.5, 1.5, (37, nb)) + rng.uniform(0, 1e-9, (37, nb))).astype(np.float64)
+        C = O.spmm(A, B)
+        assert C.dtype == np.float64
+        D = W.to_dense(A)
+        ref = D @ B
+        scale = np.abs(D) @ np.abs(B)
+        assert (np.abs(C - ref) <= 1e-12 * scale).all()
+        Bf = B.astype(np.float32).astype(np.float64)       # what an fp32 read would see
+        assert (np.abs(D @ Bf - ref) > 1e-12 * scale).any()
+        Ai = random_csr(rng, 30, 37, 0.3, dtype=np.float64, ints=True)
+        Bi = rng.integers(-4, 5, (37, nb)).astype(np.float64)
+        assert np.array_equal(O.spmm(Ai, Bi), W.to_dense(Ai) @ Bi)
+
+
+def _malformed_cases():
+    """One malformed operand per oracle_validate reject code (oracle.c, P:1675-1684 sorted levels; R10)."""
+    def csr(M, N, pos, crd):
+        crd = np.asarray(crd, np.int32)
+        return W.SparseMatrix(W.CSR, M, N, np.asarray(pos, np.int64), crd, np.ones(len(crd), np.float32))
+
+    def dcsr(M, N, outer, pos, crd):
+        crd = np.asarray(crd, np.int32)
+        return W.SparseMatrix(W.DCSR, M, N, np.asarray(pos, np.int64), crd, np.ones(len(crd), np.float32),
+                              np.asarray(outer, np.int32))
+    cases = {
+        1: csr(-1, 3, [0], []),                                  # negative size
+        3: csr(2, 3, [1, 1, 1], [0]),                            # pos[0] != 0
+        4: csr(2, 3, [0, 1, 1], [0, 2]),                         # pos[nouter] != nnz
+        5: csr(3, 3, [0, 2, 1, 2], [0, 1]),                      # pos decreasing
+        6: csr(2, 3, [0, 1, 2], [0, 3]),                         # crd >= ncols
+        7: csr(2, 3, [0, 2, 2], [1, 1]),                         # crd not strictly increasing in a row
+        8: dcsr(4, 3, [5], [0, 1], [0]),                         # stored row coordinate >= nrows
+        9: dcsr(4, 3, [2, 2], [0, 1, 2], [0, 1]),                # stored rows not strictly increasing
+        10: dcsr(4, 3, [1, 2], [0, 0, 1], [0]),                  # empty stored row (R10)
+    }
+    bad_nouter = csr(3, 3, [0, 1, 2], [0, 1])                    # CSR with nouter != nrows
+    cases[2] = bad_nouter
+    neg = csr(2, 3, [0, 1, 2], [0, -1])                          # negative crd -> also code 6
+    return cases, neg
+
+
+def test_validate_reject_codes():
+    cases, neg = _malformed_cases()
+    assert sorted(cases) == list(range(1, 11))
+    for code, A in cases.items():
+        assert O.validate(A) == code, (code, O.validate(A))
+    assert O.validate(neg) == 6
+    ok = W.from_coo([0, 0, 2], [1, 2, 0], [1.0, 2.0, 3.0], 3, 3)
+    assert O.validate(ok) == 0
+    okd = W.from_coo([0, 0, 2], [1, 2, 0], [1.0, 2.0, 3.0], 3, 3, fmt=W.DCSR)
+    assert O.validate(okd) == 0
