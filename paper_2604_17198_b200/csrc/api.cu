@@ -1,5 +1,7 @@
 // api.cu -- the C ABI of libnacho.so (include/nacho.h): host-side validation, workspace carving
 // and kernel launches.  Every numeric step runs in the kernels of the included headers.
+#include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -9,6 +11,8 @@
 #include "partition.cuh"
 #include "spadd.cuh"
 #include "spadd4.cuh"
+#include "spadd5.cuh"
+#include "spadd6.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
 #include "spmv3.cuh"
@@ -53,6 +57,20 @@ constexpr int kSpmmWitems = 128;  // 1024 positions per CTA
 constexpr int kPartWarps = NACHO_PART_WARPS;
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// The > 48 KB dynamic shared-memory opt-in is a per-device function attribute: set it once per
+// device (bit d of `done`), race-free across host threads (setting it twice is harmless).
+template <typename F>
+nacho_status smem_optin(F kern, size_t smem, std::atomic<uint64_t>& done, const char* name) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(NACHO_ERR_CUDA, "cudaGetDevice");
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return NACHO_SUCCESS;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(%s)", name);
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return NACHO_SUCCESS;
+}
 
 int64_t spmv_tile(int dtype) { return dtype == NACHO_F64 ? sv3_tile<double>() : sv3_tile<float>(); }  // = spmv3 tile
 
@@ -213,12 +231,8 @@ nacho_status launch_spadd(const SpaddArgs<T>& a, cudaStream_t st) {
   auto kern = spadd_kernel<T, FILL, kSpaddThreads, kSpaddTile>;
   const size_t smem = ((sizeof(SpaddShared<kSpaddThreads>) + 15) & ~size_t(15)) + 3 * kSpaddTile * 8 +
                       (FILL ? 3 * kSpaddTile * sizeof(T) : 0);
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(spadd_kernel)");
-    configured = true;
-  }
+  static std::atomic<uint64_t> done{0};
+  NACHO_TRY(smem_optin(kern, smem, done, "spadd_kernel"));
   kern<<<a.parts.P, kSpaddThreads, smem, st>>>(a);
   return launched(FILL ? "spadd_fill_kernel" : "spadd_count_kernel");
 }
@@ -227,12 +241,8 @@ template <typename T, int MODE, int KM, bool CHK>
 nacho_status launch_spadd4_k(const Spadd4Args<T>& a, cudaStream_t st, int64_t grid) {
   auto kern = spadd4_kernel<T, MODE, KM, CHK>;
   const size_t smem = sizeof(S4Shared<T, s4_small(MODE, KM)>);
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return fail(NACHO_ERR_CUDA, "cudaFuncSetAttribute(spadd4_kernel)");
-    configured = true;
-  }
+  static std::atomic<uint64_t> done{0};
+  NACHO_TRY(smem_optin(kern, smem, done, "spadd4_kernel"));
   kern<<<(unsigned)grid, kS4Threads, smem, st>>>(a);
   return launched(MODE == kS4Count ? "spadd4_count" : MODE == kS4Fill ? "spadd4_fill" : MODE == kS4Fused ? "spadd4_fused" : "spadd4_stage");
 }
@@ -394,6 +404,74 @@ nacho_status run_spadd_staged(const nacho_matrix* ops, int32_t k, const nacho_pa
   return launched("s4_place_kernel");
 }
 
+// Single-read SpAdd (spadd5.cuh): key column bits and the rows per sub-tile.
+int s5_cb(int64_t ncols) {
+  int cb = 1;
+  while (cb < 31 && (int64_t(1) << cb) < ncols) ++cb;
+  return cb;
+}
+
+bool spadd5_applies(const nacho_matrix* ops, int32_t k, const PartsArg& pa, cudaStream_t st) {
+  if (s5_cb(ops[0].ncols) > 24) return false;   // < 256 rows per sub-tile: the spadd4 path
+  return max_part_work(ops, k, pa, s5_max_entries(k), st) <= s5_max_entries(k);
+}
+
+template <typename T, int K>
+nacho_status launch_spadd5_k(const S5Args<T>& a, cudaStream_t st) {
+#ifdef NACHO_SPADD5   // one CTA per partition (spadd5.cuh)
+  auto kern = spadd5_kernel<T, K>;
+  const size_t smem = sizeof(S5Smem<T, K>);
+  static std::atomic<uint64_t> done{0};
+  NACHO_TRY(smem_optin(kern, smem, done, "spadd5_kernel"));
+  kern<<<(unsigned)a.parts.P, kS5Threads, smem, st>>>(a);
+  return launched("spadd5_kernel");
+#else                 // persistent, warp-specialised (spadd6.cuh): grid = resident CTAs
+  auto kern = spadd6_kernel<T, K>;
+  const size_t smem = sizeof(S6Smem<T, K>);
+  static std::atomic<uint64_t> done{0};
+  NACHO_TRY(smem_optin(kern, smem, done, "spadd6_kernel"));
+  int dev = 0, sms = 0, per = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kS6Threads, smem) != cudaSuccess || per < 1)
+    return fail(NACHO_ERR_CUDA, "spadd6 occupancy query");
+  const int64_t grid = std::min<int64_t>(a.parts.P, (int64_t)sms * per);
+  kern<<<(unsigned)grid, kS6Threads, smem, st>>>(a);
+  return launched("spadd6_kernel");
+#endif
+}
+
+template <typename T>
+nacho_status run_spadd5(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off, int64_t* z_pos,
+                        int32_t* z_crd, T* z_val, unsigned long long* state, cudaStream_t st) {
+  S5Args<T> a;
+  a.ops = make_ops(ops, k);
+  a.parts = parts_arg(parts);
+  a.cb = s5_cb(ops[0].ncols);
+  const int64_t lm = (int64_t(1) << (32 - a.cb)) - 1;
+  a.lmax = (int32_t)(lm < kS5LMax ? lm : kS5LMax);
+  a.use_bulk = 1;
+  for (int o = 0; o < k; ++o)
+    if (reinterpret_cast<uintptr_t>(ops[o].crd) % 16 || reinterpret_cast<uintptr_t>(ops[o].val) % 16) a.use_bulk = 0;
+  a.state = state;
+  a.part_off = part_off;
+  a.z_pos = z_pos;
+  a.z_crd = z_crd;
+  a.z_val = z_val;
+  if (cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (parts->P + 1), st) != cudaSuccess)
+    return fail(NACHO_ERR_CUDA, "memset look-back states");
+  switch (k) {
+    case 1: return launch_spadd5_k<T, 1>(a, st);
+    case 2: return launch_spadd5_k<T, 2>(a, st);
+    case 3: return launch_spadd5_k<T, 3>(a, st);
+    case 4: return launch_spadd5_k<T, 4>(a, st);
+    case 5: return launch_spadd5_k<T, 5>(a, st);
+    case 6: return launch_spadd5_k<T, 6>(a, st);
+    case 7: return launch_spadd5_k<T, 7>(a, st);
+    default: return launch_spadd5_k<T, 8>(a, st);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -442,7 +520,7 @@ int32_t nacho_auto_partitions(const nacho_matrix* ops, int32_t k, int32_t op) {
   if (!ops || k < 1) return 1;
   const int64_t work = total_cost(ops, k);
   if (op == 0) return auto_p(work, spmv_tile(ops[0].dtype));
-  if (op == 1) return auto_p(work, kS4Tile - (k - 1));
+  if (op == 1) return auto_p(work, s5_max_entries(k) - (k - 1));
   return auto_p(work, kSpmmWarps * kSpmmWitems);
 }
 
@@ -550,11 +628,16 @@ nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts
   if (!z_pos) return fail(NACHO_ERR_INVALID_ARG, "null z_pos");
   if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (!fits_sa_tile(ops, k, parts, st))
-    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kS4Tile);
   const size_t need = nacho_spadd_k_workspace_size(ops, k, parts->P);
   if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   auto* flags = static_cast<unsigned long long*>(ws);
+  if (spadd5_applies(ops, k, parts_arg(parts), st)) {
+    if (ops[0].dtype == NACHO_F64)
+      return run_spadd5<double>(ops, k, parts, part_off, z_pos, z_crd, static_cast<double*>(z_val), flags, st);
+    return run_spadd5<float>(ops, k, parts, part_off, z_pos, z_crd, static_cast<float*>(z_val), flags, st);
+  }
+  if (!fits_sa_tile(ops, k, parts, st))
+    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries: use the two-pass calls", kS4Tile);
   if (cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * (parts->P + 1), st) != cudaSuccess)
     return fail(NACHO_ERR_CUDA, "memset look-back flags");
   if (ops[0].dtype == NACHO_F64) {
