@@ -30,6 +30,7 @@ def build_nacho(force=False, verbose=False):
     srcs = _sources(os.path.join(HERE, "csrc")) + [os.path.join(ROOT, "include", "nacho.h")]
     if force or _newer(out, srcs):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
+               f"--split-compile={max(1, min(16, os.cpu_count() or 1))}",   # device code optimised in parallel
                "-I", os.path.join(ROOT, "include"), "-o", out, os.path.join(HERE, "csrc", "api.cu")]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

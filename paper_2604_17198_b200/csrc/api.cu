@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -13,6 +14,7 @@
 #include "spadd4.cuh"
 #include "spadd5.cuh"
 #include "spadd6.cuh"
+#include "spadd7.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
 #include "spmv3.cuh"
@@ -472,6 +474,76 @@ nacho_status run_spadd5(const nacho_matrix* ops, int32_t k, const nacho_parts* p
   }
 }
 
+// Pipelined single-read SpAdd (spadd7.cuh): producer / compute / emission warps over NS stages.
+template <typename T, int K>
+nacho_status launch_spadd7_k(const S7Args<T>& a, cudaStream_t st) {
+  auto kern = spadd7_kernel<T, K>;
+  const size_t smem = sizeof(S7Smem<T, K>);
+  static std::atomic<uint64_t> done{0};
+  NACHO_TRY(smem_optin(kern, smem, done, "spadd7_kernel"));
+  int dev = 0, sms = 0, per = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kS7Threads, smem) != cudaSuccess || per < 1)
+    return fail(NACHO_ERR_CUDA, "spadd7 occupancy query");
+  const int64_t grid = std::min<int64_t>(a.parts.P, (int64_t)sms * per);
+  kern<<<(unsigned)grid, kS7Threads, smem, st>>>(a);
+  return launched("spadd7_kernel");
+}
+
+template <typename T>
+nacho_status run_spadd7(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off, int64_t* z_pos,
+                        int32_t* z_crd, T* z_val, unsigned long long* state, cudaStream_t st) {
+  S7Args<T> a;
+  memset(&a, 0, sizeof(a));
+  a.ops = make_ops(ops, k);
+  a.parts = parts_arg(parts);
+  a.cb = s5_cb(ops[0].ncols);
+  a.ndist = 0;
+  a.use_bulk = 1;
+  for (int o = 0; o < k; ++o) {
+    int d = 0;
+    while (d < a.ndist && a.dpos[d] != ops[o].pos) ++d;   // operands sharing one pos array: one copy
+    if (d == a.ndist) a.dpos[a.ndist++] = ops[o].pos;
+    a.pd[o] = d;
+    if (reinterpret_cast<uintptr_t>(ops[o].crd) % 16 || reinterpret_cast<uintptr_t>(ops[o].val) % 16 ||
+        reinterpret_cast<uintptr_t>(ops[o].pos) % 16)
+      a.use_bulk = 0;
+  }
+  a.sp = (kS7PosPool / a.ndist) & ~1;
+  int64_t lm = (int64_t(1) << (32 - a.cb)) - 2;
+  if (lm > a.sp - 2) lm = a.sp - 2;
+  if (lm > kS7LMax) lm = kS7LMax;
+  a.lmax = (int32_t)lm;
+  a.state = state;
+  a.part_off = part_off;
+  a.z_pos = z_pos;
+  a.z_crd = z_crd;
+  a.z_val = z_val;
+  if (cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (parts->P + 2), st) != cudaSuccess)
+    return fail(NACHO_ERR_CUDA, "memset look-back states");
+  switch (k) {
+    case 1: return launch_spadd7_k<T, 1>(a, st);
+    case 2: return launch_spadd7_k<T, 2>(a, st);
+    case 3: return launch_spadd7_k<T, 3>(a, st);
+    case 4: return launch_spadd7_k<T, 4>(a, st);
+    case 5: return launch_spadd7_k<T, 5>(a, st);
+    case 6: return launch_spadd7_k<T, 6>(a, st);
+    case 7: return launch_spadd7_k<T, 7>(a, st);
+    default: return launch_spadd7_k<T, 8>(a, st);
+  }
+}
+
+// Which single-read kernel nacho_spadd_k runs: 7 (pipelined, default) or 6 (NACHO_SPADD_IMPL=6;
+// A/B comparisons only).
+int spadd_impl() {
+  static const int impl = [] {
+    const char* e = getenv("NACHO_SPADD_IMPL");
+    return e && e[0] == '6' ? 6 : 7;
+  }();
+  return impl;
+}
+
 }  // namespace
 
 extern "C" {
@@ -559,7 +631,7 @@ nacho_status nacho_spmv(const nacho_matrix* A, const nacho_parts* parts, const v
 
 size_t nacho_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {
   (void)ops; (void)k;
-  return align_up((size_t)((P > 0 ? P : 1) + 1) * 8);
+  return align_up((size_t)((P > 0 ? P : 1) + 2) * 8);   // look-back states, ticket, error flag
 }
 
 nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
@@ -632,6 +704,11 @@ nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts
   if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
   auto* flags = static_cast<unsigned long long*>(ws);
   if (spadd5_applies(ops, k, parts_arg(parts), st)) {
+    if (spadd_impl() == 7) {
+      if (ops[0].dtype == NACHO_F64)
+        return run_spadd7<double>(ops, k, parts, part_off, z_pos, z_crd, static_cast<double*>(z_val), flags, st);
+      return run_spadd7<float>(ops, k, parts, part_off, z_pos, z_crd, static_cast<float*>(z_val), flags, st);
+    }
     if (ops[0].dtype == NACHO_F64)
       return run_spadd5<double>(ops, k, parts, part_off, z_pos, z_crd, static_cast<double*>(z_val), flags, st);
     return run_spadd5<float>(ops, k, parts, part_off, z_pos, z_crd, static_cast<float*>(z_val), flags, st);
