@@ -520,7 +520,12 @@ nacho_status run_spadd7(const nacho_matrix* ops, int32_t k, const nacho_parts* p
   a.z_pos = z_pos;
   a.z_crd = z_crd;
   a.z_val = z_val;
-  if (cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (parts->P + 2), st) != cudaSuccess)
+#ifdef NACHO_S7_PROF
+  const int nclear = parts->P + 2 + 16;
+#else
+  const int nclear = parts->P + 2;
+#endif
+  if (cudaMemsetAsync(state, 0, sizeof(unsigned long long) * nclear, st) != cudaSuccess)
     return fail(NACHO_ERR_CUDA, "memset look-back states");
   switch (k) {
     case 1: return launch_spadd7_k<T, 1>(a, st);
@@ -631,6 +636,9 @@ nacho_status nacho_spmv(const nacho_matrix* A, const nacho_parts* parts, const v
 
 size_t nacho_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {
   (void)ops; (void)k;
+#ifdef NACHO_S7_PROF
+  return align_up((size_t)((P > 0 ? P : 1) + 2 + 16) * 8);   // + profiling counters (dev builds)
+#endif
   return align_up((size_t)((P > 0 ? P : 1) + 2) * 8);   // look-back states, ticket, error flag
 }
 

@@ -90,8 +90,18 @@ struct S7Smem {
   int32_t ML[kS7LMax + 1];        // merged position of each owned row's first entry
   int32_t wred[kS7Compute / 32];
   int64_t run_off;
+  int64_t excl[S7Cfg<V, K>::NS];     // emission -> compute: exclusive prefix of the stage's job
+  int32_t excl_ok[S7Cfg<V, K>::NS];  // ... once resolved (reset by the emission after the job)
   uint64_t full[S7Cfg<V, K>::NS], done[S7Cfg<V, K>::NS], empty[S7Cfg<V, K>::NS];
 };
+
+#ifdef NACHO_S7_PROF   // dev builds: cycles per role and wait, accumulated at state[P + 2 + i]
+#define S7_T0() const long long _t0 = clock64()
+#define S7_ACC(i) atomicAdd(a.state + a.parts.P + 2 + (i), (unsigned long long)(clock64() - _t0))
+#else
+#define S7_T0()
+#define S7_ACC(i)
+#endif
 
 __device__ __forceinline__ void s7_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
@@ -133,7 +143,11 @@ __device__ __forceinline__ void s7_produce(const S7Args<V>& a, S7Smem<V, K>& sh)
     const int s = njob % NS;
     const uint32_t ph = (uint32_t)(njob / NS) & 1u;
     ++njob;
-    s7_wait_sleep(&sh.empty[s], ph ^ 1u, 256);
+    {
+      S7_T0();
+      s7_wait_sleep(&sh.empty[s], ph ^ 1u, 256);
+      if (lane == 0) S7_ACC(0);   // producer: waiting for a free stage
+    }
     S7Stage<V, K>& g = sh.st[s];
     int64_t sv[K], ev[K];
     int soff[K], nn[K], base[K + 1];
@@ -157,7 +171,12 @@ __device__ __forceinline__ void s7_produce(const S7Args<V>& a, S7Smem<V, K>& sh)
     }
     const int64_t ps = (a0 + 1) & ~int64_t(1);        // pool: rows [ps, ...) of every distinct pos array
     const int64_t pneed = a0 + lrows + 1;             // rows a0 + 1 .. a0 + lrows are read
-    const int64_t pe = lrows > 0 ? (pneed & ~int64_t(1)) : ps;
+    // bulk ranges: crd / val [s & ~3, ceil4(e)) -- the <= 3 slots past e land in the run's pad --
+    // unless ceil4(e) passes the array end (then [.., e & ~3) and plain loads of the rest); pos
+    // [ps, ceil2(pneed)) likewise
+    const int64_t pe_up = (pneed + 1) & ~int64_t(1);
+    const bool pos_up = pe_up <= a.ops.op[0].nouter + 1;
+    const int64_t pe = lrows > 0 ? (pos_up ? pe_up : (pneed & ~int64_t(1))) : ps;
     if (lane == 0) {
       g.tile = tile; g.a0 = a0; g.ps = ps; g.lrows = lrows; g.mode = mode; g.last = last;
 #pragma unroll
@@ -165,58 +184,59 @@ __device__ __forceinline__ void s7_produce(const S7Args<V>& a, S7Smem<V, K>& sh)
 #pragma unroll
       for (int o = 0; o <= K; ++o) g.base[o] = base[o];
     }
-    // entries the bulk copies do not cover (the < 4 after the last aligned group), plain loads
+    int64_t hi[K];
     uint32_t bytes = 0;
 #pragma unroll
     for (int o = 0; o < K; ++o) {
-      const OpView& op = a.ops.op[o];
       const int64_t lo = sv[o] & ~int64_t(3);
-      int64_t hi = ev[o] & ~int64_t(3);
-      if (!a.use_bulk || hi <= sv[o]) hi = lo;
-      bytes += (uint32_t)(hi - lo) * (4u + (uint32_t)sizeof(V));
-      const int64_t from = hi > lo ? hi : sv[o];
-      for (int64_t q = from + lane; q < ev[o]; q += 32) {
-        const int slot = soff[o] + (int)(q - sv[o]);
-        g.key[slot] = (uint32_t)ldg(op.crd + q);
-        g.val[slot] = ldg(static_cast<const V*>(op.val) + q);
-      }
+      const int64_t up = (ev[o] + 3) & ~int64_t(3);
+      hi[o] = up <= a.ops.op[o].nnz ? up : (ev[o] & ~int64_t(3));
+      if (!a.use_bulk || hi[o] <= sv[o]) hi[o] = lo;
+      bytes += (uint32_t)(hi[o] - lo) * (4u + (uint32_t)sizeof(V));
     }
-    if (lrows > 0) {
-      bytes += (uint32_t)(pe - ps) * 8u * (uint32_t)a.ndist;
-      if (pneed > pe || !a.use_bulk) {   // rows past the last aligned pair (or every row)
-        for (int d = 0; d < a.ndist; ++d)
-          for (int64_t r = (a.use_bulk ? pe : ps) + lane; r < pneed; r += 32) g.pos[d * a.sp + (int)(r - ps)] = ldg(a.dpos[d] + r);
-      }
-      if (!a.use_bulk) bytes -= (uint32_t)(pe - ps) * 8u * (uint32_t)a.ndist;
-    }
+    const bool pcopy = a.use_bulk && lrows > 0 && pe > ps;
+    if (pcopy) bytes += (uint32_t)(pe - ps) * 8u * (uint32_t)a.ndist;
+    // 1. the transaction bytes, then the copies (one per lane: crd of operand o at lane o, val at
+    //    lane K + o, pos of distinct array d at lane 2K + d) -- nothing waits on global memory first
+    if (lane == 0 && bytes) mbar_expect_tx(&sh.full[s], bytes);
     __syncwarp();
-    if (lane == 0) {
-      fence_proxy_async();
-      if (bytes) mbar_arrive_expect_tx(&sh.full[s], bytes);
-      else mbar_arrive(&sh.full[s]);
-    }
-    __syncwarp();
-    if (bytes) {   // one copy per lane: crd of operand o (lane o), val (lane K + o), pos (lane 2K + d)
-      if (lane < 2 * K) {
-        const int o = lane < K ? lane : lane - K;
-        int64_t so2 = 0, eo2 = 0;
-        int bo = 0;
+    if (lane < 2 * K) {
+      const int o = lane < K ? lane : lane - K;
+      int64_t so2 = 0, hi2 = 0;
+      int bo = 0;
 #pragma unroll
-        for (int oo = 0; oo < K; ++oo) if (oo == o) { so2 = sv[oo]; eo2 = ev[oo]; bo = base[oo]; }
-        const int64_t lo = so2 & ~int64_t(3);
-        const int64_t hi = eo2 & ~int64_t(3);
-        if (a.use_bulk && hi > so2) {
-          const OpView& op = a.ops.op[o];
-          const uint32_t nb = (uint32_t)(hi - lo);
-          if (lane < K) bulk_g2s(g.key + bo, op.crd + lo, nb * 4u, &sh.full[s]);
-          else bulk_g2s(g.val + bo, static_cast<const V*>(op.val) + lo, nb * (uint32_t)sizeof(V), &sh.full[s]);
+      for (int oo = 0; oo < K; ++oo) if (oo == o) { so2 = sv[oo]; hi2 = hi[oo]; bo = base[oo]; }
+      const int64_t lo = so2 & ~int64_t(3);
+      if (hi2 > lo) {
+        const OpView& op = a.ops.op[o];
+        const uint32_t nb = (uint32_t)(hi2 - lo);
+        if (lane < K) bulk_g2s(g.key + bo, op.crd + lo, nb * 4u, &sh.full[s]);
+        else bulk_g2s(g.val + bo, static_cast<const V*>(op.val) + lo, nb * (uint32_t)sizeof(V), &sh.full[s]);
+      }
+    } else if (lane < 2 * K + a.ndist) {
+      const int d = lane - 2 * K;
+      if (pcopy) bulk_g2s(g.pos + d * a.sp, a.dpos[d] + ps, (uint32_t)(pe - ps) * 8u, &sh.full[s]);
+    }
+    // 2. entries the copies do not cover (array ends, unaligned bases): plain loads
+#pragma unroll
+    for (int o = 0; o < K; ++o) {
+      const int64_t from = hi[o] > (sv[o] & ~int64_t(3)) ? hi[o] : sv[o];
+      if (from < ev[o]) {
+        const OpView& op = a.ops.op[o];
+        for (int64_t q = from + lane; q < ev[o]; q += 32) {
+          const int slot = soff[o] + (int)(q - sv[o]);
+          g.key[slot] = (uint32_t)ldg(op.crd + q);
+          g.val[slot] = ldg(static_cast<const V*>(op.val) + q);
         }
-      } else if (lane < 2 * K + a.ndist) {
-        const int d = lane - 2 * K;
-        if (a.use_bulk && lrows > 0 && pe > ps)
-          bulk_g2s(g.pos + d * a.sp, a.dpos[d] + ps, (uint32_t)(pe - ps) * 8u, &sh.full[s]);
       }
     }
+    if (lrows > 0 && (!pcopy || pe < pneed)) {
+      for (int d = 0; d < a.ndist; ++d)
+        for (int64_t r = (pcopy ? pe : ps) + lane; r < pneed; r += 32) g.pos[d * a.sp + (int)(r - ps)] = ldg(a.dpos[d] + r);
+    }
+    // 3. the arrival: releases the record and the plain stores; the phase completes with the copies
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.full[s]);
   };
   fetch();
   for (;;) {
@@ -256,11 +276,31 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
   const int P = a.parts.P;
   for (int njob = 0;; ++njob) {
     const int s = njob % NS;
-    s7_wait_sleep(&sh.done[s], (uint32_t)(njob / NS) & 1u, 64);
+    const uint32_t ph = (uint32_t)(njob / NS) & 1u;
+    // the look-back of a one-pass job runs while the compute warps merge it: it needs only the
+    // predecessors' states, so it starts as soon as the job record is in the stage
+    s7_wait_sleep(&sh.full[s], ph, 64);
     S7Stage<V, K>& g = sh.st[s];
     const int64_t t = g.tile;
-    if (t < 0) break;
     const int mode = g.mode;
+    int64_t excl = 0;
+    if (t > 0 && mode == 1) {
+      S7_T0();
+      excl = s5_lookback(a.state, t);
+      if (lane == 0) S7_ACC(2);   // emission: look-back
+    }
+    if (lane == 0) {   // the compute warps publish the inclusive prefix at once if it is known
+      sh.excl[s] = excl;
+      __threadfence_block();
+      *reinterpret_cast<volatile int*>(&sh.excl_ok[s]) = 1;
+    }
+    {
+      S7_T0();
+      s7_wait_sleep(&sh.done[s], ph, 64);
+      if (lane == 0) S7_ACC(1);   // emission: waiting for a computed stage
+    }
+    if (lane == 0) sh.excl_ok[s] = 0;
+    if (t < 0) break;
     if (mode != 0) {
       const int total = g.total, lrows = g.lrows;
       const int64_t a0 = g.a0;
@@ -268,7 +308,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
       if (mode == 2) {
         off = g.off;
       } else {
-        off = t > 0 ? s5_lookback(a.state, t) : 0;
+        off = excl;
         if (lane == 0) {
           if (t > 0) st_release(a.state + t, kS5Incl | (unsigned long long)(off + total));
           if (a.part_off) {
@@ -292,6 +332,107 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
   }
 }
 
+// ------------------------------------------------------------------ one-row jobs: bitmap union
+// A job inside one row whose columns span at most s7_bw<K>() words (most partitions of a power-law
+// matrix's heavy rows): per-operand column bitmaps (one atomic OR per entry), the union bitmap's
+// exclusive popcount prefix gives every union column its output index, and the values fold into
+// that slot operand by operand -- the left fold in operand order from the first present value
+// (R9) -- so no keys and no merge stages.  Returns the union size; with `emit` the union (column,
+// value) is written at [0, total) of the stage's key / val arrays (inputs are held in registers).
+template <int K>
+__host__ __device__ constexpr int s7_bw() { return (3 * (kS7Slots + 16) / 2 - 8) / (K + 2); }
+
+template <typename V, int K>
+__device__ __forceinline__ int s7_bitmap(S7Stage<V, K>& g, S7Smem<V, K>& sh, int cmin, int nw, int S, bool emit) {
+  const int tid = threadIdx.x;
+  uint32_t* bm = sh.key1;              // [K][nw] operand bitmaps, then U[nw] union, pre[nw + 1]
+  uint32_t* U = bm + K * nw;
+  uint32_t* pre = U + nw;
+  for (int w = tid; w < K * nw; w += kS7Compute) bm[w] = 0;
+  if (tid < 8 * K) {   // pad slots of every run (<= 3 before, <= 4 after it) -> ~0u: not an entry
+    const int o = tid >> 3, j = tid & 7;
+    const int z = j < 4 ? g.base[o] + j : g.soff[o] + g.n[o] + (j - 4);
+    if ((j < 4 && z < g.soff[o]) || (j >= 4 && z < g.base[o + 1])) g.key[z] = ~0u;
+  }
+  s6_sync();   // bitmaps zeroed, pads marked
+  // slots d .. d + 7 (consecutive: mostly one operand, sorted columns): the bits of one word are
+  // combined in registers, one atomic OR per distinct word (1-2 per thread on dense rows)
+  const int d = tid * kS5VT;
+  uint32_t c[kS5VT];
+  V v[kS5VT];
+  int oo[kS5VT];   // operand of the slot, -1: not an entry
+  {
+    const uint4 c0 = reinterpret_cast<const uint4*>(g.key + d)[0];
+    const uint4 c1 = reinterpret_cast<const uint4*>(g.key + d)[1];
+    c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w; c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
+  }
+  uint32_t cw = ~0u, cbits = 0;
+#pragma unroll
+  for (int i = 0; i < kS5VT; ++i) {
+    const int slot = d + i;
+    int o = 0;
+#pragma unroll
+    for (int q = 1; q < K; ++q) o += slot >= g.base[q] ? 1 : 0;
+    const bool ok = slot < S && c[i] != ~0u;
+    oo[i] = ok ? o : -1;
+    v[i] = ok ? g.val[slot] : V(0);
+    c[i] -= (uint32_t)cmin;
+    if (ok) {
+      const uint32_t w = (uint32_t)(o * nw) + (c[i] >> 5);
+      if (w != cw) {
+        if (cw != ~0u) atomicOr(&bm[cw], cbits);
+        cw = w;
+        cbits = 0;
+      }
+      cbits |= 1u << (c[i] & 31);
+    }
+  }
+  if (cw != ~0u) atomicOr(&bm[cw], cbits);
+  s6_sync();
+  // union words and their exclusive popcount prefix (each thread a contiguous run of words)
+  const int wpt = (nw + kS7Compute - 1) / kS7Compute;
+  const int w0 = tid * wpt;
+  int cnt = 0;
+  for (int w = w0; w < w0 + wpt && w < nw; ++w) {
+    uint32_t u = 0;
+#pragma unroll
+    for (int q = 0; q < K; ++q) u |= bm[q * nw + w];
+    U[w] = u;
+    cnt += __popc(u);
+  }
+  int total;
+  int run = s6_block_excl(cnt, sh.wred, &total);
+  for (int w = w0; w < w0 + wpt && w < nw; ++w) {
+    pre[w] = (uint32_t)run;
+    run += __popc(U[w]);
+  }
+  if (!emit) return total;
+  s6_sync();
+  // values fold operand by operand (one phase per operand: distinct output slots within a phase)
+#pragma unroll
+  for (int o = 0; o < K; ++o) {
+#pragma unroll
+    for (int i = 0; i < kS5VT; ++i) {
+      if (oo[i] == o) {
+        const int w = (int)(c[i] >> 5);
+        const uint32_t bit = c[i] & 31;
+        const int idx = (int)pre[w] + __popc(U[w] & ((1u << bit) - 1u));
+        uint32_t lower = 0;
+#pragma unroll
+        for (int q = 0; q < K; ++q) if (q < o) lower |= bm[q * nw + w];
+        if ((lower >> bit) & 1u) {
+          g.val[idx] = g.val[idx] + v[i];
+        } else {
+          g.key[idx] = c[i] + (uint32_t)cmin;
+          g.val[idx] = v[i];
+        }
+      }
+    }
+    if (o + 1 < K) s6_sync();
+  }
+  return total;
+}
+
 // ------------------------------------------------------------------ compute warps
 template <typename V, int K>
 __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh) {
@@ -301,7 +442,11 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
   int64_t cnt_total = 0, run_off = 0;
   for (int njob = 0;; ++njob) {
     const int s = njob % NS;
-    s7_wait(&sh.full[s], (uint32_t)(njob / NS) & 1u);
+    {
+      S7_T0();
+      s7_wait_sleep(&sh.full[s], (uint32_t)(njob / NS) & 1u, 32);
+      if (tid == 0) S7_ACC(3);   // compute: waiting for a loaded stage
+    }
     S7Stage<V, K>& g = sh.st[s];
     const int64_t t = g.tile;
     if (t < 0) {
@@ -312,129 +457,153 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
     const int last = g.last;   // read before the union count: tid 0 may free the stage right after it
     const int S = g.base[K];
     const int lrows = g.lrows;
-    // ---- partition-local row of every slot (multi-row jobs only), keys in place, run sentinels
-    if (lrows > 0) {
-      for (int c = tid; c < (S >> 2); c += kS7Compute) {   // mark (o << 16) | 0: operand o, local row 0
-        const int slot = c << 2;
-        uint32_t o = 0;
+    // ---- one-row job with a narrow column span: the bitmap union
+    int cmin = INT32_MAX, cmax = -1;
+    if (lrows == 0) {
 #pragma unroll
-        for (int oo = 1; oo < K; ++oo) o += slot >= g.base[oo] ? 1u : 0u;
-        const uint32_t m = o << 16;
-        reinterpret_cast<uint4*>(sh.key1)[c] = make_uint4(m, m, m, m);
-      }
-      s6_sync();
-      const int64_t pb = g.a0 - g.ps;
-      for (int l = tid + 1; l <= lrows; l += kS7Compute) {   // first entry of rows 1 .. lrows
-        int msum = 0;
-#pragma unroll
-        for (int o = 0; o < K; ++o) {
-          const int64_t* pp = g.pos + a.pd[o] * a.sp + (pb + l);
-          const int64_t so = g.s[o], eo = g.e[o];
-          const int64_t p = min(pp[0], eo);
-          const int64_t pn = l < lrows ? min(pp[1], eo) : eo;
-          const int rel = (int)(p - so);
-          msum += rel;
-          if (pn > p) sh.key1[g.soff[o] + rel] = ((uint32_t)o << 16) | (uint32_t)l;
-        }
-        sh.ML[l] = msum;
-      }
-      s6_sync();
-      const int d = tid * kS5VT;
-      uint32_t m[kS5VT];
-      const uint4 m0 = reinterpret_cast<const uint4*>(sh.key1 + d)[0];
-      const uint4 m1 = reinterpret_cast<const uint4*>(sh.key1 + d)[1];
-      m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
-#pragma unroll
-      for (int v = 1; v < kS5VT; ++v) m[v] = max(m[v], m[v - 1]);
-      const uint32_t pre = s6_block_excl_max(m[kS5VT - 1], sh.wred);
-      if (d < S) {
-        uint4* k4 = reinterpret_cast<uint4*>(g.key + d);
-        uint4 c0 = k4[0], c1 = k4[1];
-        const int cb = a.cb;
-        auto mk = [&](uint32_t c, uint32_t mm) { return ((max(mm, pre) & 0xffffu) << cb) | c; };
-        c0.x = mk(c0.x, m[0]); c0.y = mk(c0.y, m[1]); c0.z = mk(c0.z, m[2]); c0.w = mk(c0.w, m[3]);
-        c1.x = mk(c1.x, m[4]); c1.y = mk(c1.y, m[5]); c1.z = mk(c1.z, m[6]); c1.w = mk(c1.w, m[7]);
-        k4[0] = c0;
-        k4[1] = c1;
-#pragma unroll
-        for (int o = 0; o < K; ++o) {   // the sentinel after every run, by the slot's owner
-          const int z = g.soff[o] + g.n[o];
-          if (z >= d && z < d + kS5VT) g.key[z] = kS5Inf;
+      for (int o = 0; o < K; ++o) {
+        if (g.n[o] > 0) {
+          cmin = min(cmin, (int)g.key[g.soff[o]]);
+          cmax = max(cmax, (int)g.key[g.soff[o] + g.n[o] - 1]);
         }
       }
-    } else if (tid < K) {
-      g.key[g.soff[tid] + g.n[tid]] = kS5Inf;   // the sentinel after every run (keys are the columns)
     }
-    s6_sync();
-    // ---- merge stages 1 .. K-2
-    const uint32_t* X = g.key + g.soff[0];
-    const uint16_t* XS = sh.src1;
-    const int xs0 = g.soff[0];
-    int na = g.n[0];
-#pragma unroll
-    for (int st = 1; st + 1 < K; ++st) {
-      uint32_t* OK = (st & 1) ? sh.key1 : sh.key2;
-      uint16_t* OS = (st & 1) ? sh.src1 : sh.src2;
-      if (st == 1) s5_merge_stage<false>(X, XS, xs0, na, g.key + g.soff[st], g.soff[st], g.n[st], OK, OS);
-      else s5_merge_stage<true>(X, XS, xs0, na, g.key + g.soff[st], g.soff[st], g.n[st], OK, OS);
-      s6_sync();
-      X = OK;
-      XS = OS;
-      na += g.n[st];
-    }
-    // ---- last stage: merge, fold equal keys (R9), count
-    constexpr bool XSRC = K >= 3;
-    const uint32_t* Y = K > 1 ? g.key + g.soff[K - 1] : g.key + g.soff[0] + g.n[0];
-    const int ys0 = K > 1 ? g.soff[K - 1] : 0;
-    const int nb = K > 1 ? g.n[K - 1] : 0;
-    const int n = na + nb;
+    const int nw = cmax >= cmin ? ((cmax - cmin) >> 5) + 1 : 0;
+    const bool bmp = lrows == 0 && nw > 0 && nw <= s7_bw<K>();
     const int d = tid * kS5VT;
-    const uint32_t cmask = (1u << a.cb) - 1u;
     V res[kS5VT];
     uint32_t col[kS5VT];
-    uint32_t em = 0;   // bit v: item v ends a run this thread owns (one union entry)
-    if (d < n) {
-      int i = s5_split(X, na, Y, nb, d), jj = d - i;
-      uint32_t pk = kS5Inf;
-      if (d > 0) {
-        const bool tx = i > 0 && (jj == 0 || X[i - 1] >= Y[jj - 1]);
-        pk = tx ? X[i - 1] : Y[jj - 1];
-      }
-      uint32_t xk = X[i], yk = Y[jj];
-      bool own = false;
-      V acc = V(0);
-#pragma unroll
-      for (int v = 0; v < kS5VT; ++v) {
-        uint32_t key;
-        int slot;
-        s5_step<XSRC>(X, XS, xs0, Y, ys0, i, jj, xk, yk, key, slot);
-        const bool valid = d + v < n;
-        const bool start = valid && key != pk;
-        if (v > 0 && own && (start || !valid) && d + v - 1 < n) em |= 1u << (v - 1);
-        own = own || start;
-        if (own && valid) {
-          const V x = g.val[slot];
-          acc = start ? x : acc + x;
+    uint32_t em = 0;   // merge path: bit v -- item v ends a run this thread owns (one union entry)
+    int n = 0, ex = 0, total = 0;
+#ifdef NACHO_S7_PROF
+    const long long _tc = clock64();
+#endif
+    if (bmp) {
+      total = s7_bitmap<V, K>(g, sh, cmin, nw, S, mode != 0);
+    } else {
+      // ---- partition-local row of every slot (multi-row jobs only), keys in place, run sentinels
+      if (lrows > 0) {
+        for (int c = tid; c < (S >> 2); c += kS7Compute) {   // mark (o << 16) | 0: operand o, local row 0
+          const int slot = c << 2;
+          uint32_t o = 0;
+  #pragma unroll
+          for (int oo = 1; oo < K; ++oo) o += slot >= g.base[oo] ? 1u : 0u;
+          const uint32_t m = o << 16;
+          reinterpret_cast<uint4*>(sh.key1)[c] = make_uint4(m, m, m, m);
         }
-        res[v] = acc;
-        col[v] = key & cmask;
-        pk = key;
+        s6_sync();
+        const int64_t pb = g.a0 - g.ps;
+        for (int l = tid + 1; l <= lrows; l += kS7Compute) {   // first entry of rows 1 .. lrows
+          int msum = 0;
+  #pragma unroll
+          for (int o = 0; o < K; ++o) {
+            const int64_t* pp = g.pos + a.pd[o] * a.sp + (pb + l);
+            const int64_t so = g.s[o], eo = g.e[o];
+            const int64_t p = min(pp[0], eo);
+            const int64_t pn = l < lrows ? min(pp[1], eo) : eo;
+            const int rel = (int)(p - so);
+            msum += rel;
+            if (pn > p) sh.key1[g.soff[o] + rel] = ((uint32_t)o << 16) | (uint32_t)l;
+          }
+          sh.ML[l] = msum;
+        }
+        s6_sync();
+        const int d = tid * kS5VT;
+        uint32_t m[kS5VT];
+        const uint4 m0 = reinterpret_cast<const uint4*>(sh.key1 + d)[0];
+        const uint4 m1 = reinterpret_cast<const uint4*>(sh.key1 + d)[1];
+        m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
+  #pragma unroll
+        for (int v = 1; v < kS5VT; ++v) m[v] = max(m[v], m[v - 1]);
+        const uint32_t pre = s6_block_excl_max(m[kS5VT - 1], sh.wred);
+        if (d < S) {
+          uint4* k4 = reinterpret_cast<uint4*>(g.key + d);
+          uint4 c0 = k4[0], c1 = k4[1];
+          const int cb = a.cb;
+          auto mk = [&](uint32_t c, uint32_t mm) { return ((max(mm, pre) & 0xffffu) << cb) | c; };
+          c0.x = mk(c0.x, m[0]); c0.y = mk(c0.y, m[1]); c0.z = mk(c0.z, m[2]); c0.w = mk(c0.w, m[3]);
+          c1.x = mk(c1.x, m[4]); c1.y = mk(c1.y, m[5]); c1.z = mk(c1.z, m[6]); c1.w = mk(c1.w, m[7]);
+          k4[0] = c0;
+          k4[1] = c1;
+  #pragma unroll
+          for (int o = 0; o < K; ++o) {   // the sentinel after every run, by the slot's owner
+            const int z = g.soff[o] + g.n[o];
+            if (z >= d && z < d + kS5VT) g.key[z] = kS5Inf;
+          }
+        }
+      } else if (tid < K) {
+        g.key[g.soff[tid] + g.n[tid]] = kS5Inf;   // the sentinel after every run (keys are the columns)
       }
-      if (own && d + kS5VT <= n) {   // the last run may continue past this thread's items
-        em |= 1u << (kS5VT - 1);
-#pragma unroll
-        for (int r = 0; r < K - 1; ++r) {
-          if (d + kS5VT + r >= n || (xk <= yk ? xk : yk) != pk) break;
+      s6_sync();
+      // ---- merge stages 1 .. K-2
+      const uint32_t* X = g.key + g.soff[0];
+      const uint16_t* XS = sh.src1;
+      const int xs0 = g.soff[0];
+      int na = g.n[0];
+  #pragma unroll
+      for (int st = 1; st + 1 < K; ++st) {
+        uint32_t* OK = (st & 1) ? sh.key1 : sh.key2;
+        uint16_t* OS = (st & 1) ? sh.src1 : sh.src2;
+        if (st == 1) s5_merge_stage<false>(X, XS, xs0, na, g.key + g.soff[st], g.soff[st], g.n[st], OK, OS);
+        else s5_merge_stage<true>(X, XS, xs0, na, g.key + g.soff[st], g.soff[st], g.n[st], OK, OS);
+        s6_sync();
+        X = OK;
+        XS = OS;
+        na += g.n[st];
+      }
+      // ---- last stage: merge, fold equal keys (R9), count
+      constexpr bool XSRC = K >= 3;
+      const uint32_t* Y = K > 1 ? g.key + g.soff[K - 1] : g.key + g.soff[0] + g.n[0];
+      const int ys0 = K > 1 ? g.soff[K - 1] : 0;
+      const int nb = K > 1 ? g.n[K - 1] : 0;
+      n = na + nb;
+      const uint32_t cmask = (1u << a.cb) - 1u;
+      if (d < n) {
+        int i = s5_split(X, na, Y, nb, d), jj = d - i;
+        uint32_t pk = kS5Inf;
+        if (d > 0) {
+          const bool tx = i > 0 && (jj == 0 || X[i - 1] >= Y[jj - 1]);
+          pk = tx ? X[i - 1] : Y[jj - 1];
+        }
+        uint32_t xk = X[i], yk = Y[jj];
+        bool own = false;
+        V acc = V(0);
+  #pragma unroll
+        for (int v = 0; v < kS5VT; ++v) {
           uint32_t key;
           int slot;
           s5_step<XSRC>(X, XS, xs0, Y, ys0, i, jj, xk, yk, key, slot);
-          acc = acc + g.val[slot];
+          const bool valid = d + v < n;
+          const bool start = valid && key != pk;
+          if (v > 0 && own && (start || !valid) && d + v - 1 < n) em |= 1u << (v - 1);
+          own = own || start;
+          if (own && valid) {
+            const V x = g.val[slot];
+            acc = start ? x : acc + x;
+          }
+          res[v] = acc;
+          col[v] = key & cmask;
+          pk = key;
         }
-        res[kS5VT - 1] = acc;
+        if (own && d + kS5VT <= n) {   // the last run may continue past this thread's items
+          em |= 1u << (kS5VT - 1);
+  #pragma unroll
+          for (int r = 0; r < K - 1; ++r) {
+            if (d + kS5VT + r >= n || (xk <= yk ? xk : yk) != pk) break;
+            uint32_t key;
+            int slot;
+            s5_step<XSRC>(X, XS, xs0, Y, ys0, i, jj, xk, yk, key, slot);
+            acc = acc + g.val[slot];
+          }
+          res[kS5VT - 1] = acc;
+        }
       }
+      ex = s6_block_excl(__popc(em), sh.wred, &total);   // syncs: every merge / fold is done
     }
-    int total;
-    const int ex = s6_block_excl(__popc(em), sh.wred, &total);   // syncs: every merge / fold is done
+#ifdef NACHO_S7_PROF
+    if (tid == 0) atomicAdd(a.state + a.parts.P + 2 + (bmp ? 4 : 5), (unsigned long long)(clock64() - _tc));
+    if (tid == 0) atomicAdd(a.state + a.parts.P + 2 + (bmp ? 6 : 7), 1ull);
+#endif
     if (mode == 0) {   // count a sub-tile; after the last one: publish, look back, known offset
       cnt_total += total;
       if (last) {
@@ -463,13 +632,19 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
       continue;
     }
     if (tid == 0) {
-      if (mode == 1) st_release(a.state + t, (t == 0 ? kS5Incl : kS5Agg) | (unsigned long long)total);
+      if (mode == 1) {   // inclusive prefix if the early look-back is done, else the aggregate
+        const bool known = t == 0 || *reinterpret_cast<volatile int*>(&sh.excl_ok[s]) != 0;
+        __threadfence_block();
+        const unsigned long long v = known ? kS5Incl | (unsigned long long)(sh.excl[s] + total)
+                                           : kS5Agg | (unsigned long long)total;
+        st_release(a.state + t, t == 0 ? kS5Incl | (unsigned long long)total : v);
+      }
       else g.off = run_off;
       g.total = total;
     }
     if (mode == 2) run_off += total;
     // ---- the compacted union into the stage, and the union count before each owned row
-    if (d < n) {
+    if (!bmp && d < n) {
       int e = ex;
 #pragma unroll
       for (int v = 0; v < kS5VT; ++v) {
@@ -477,7 +652,7 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
         if (em & (1u << v)) { g.key[e] = col[v]; g.val[e] = res[v]; ++e; }
       }
     }
-    if (tid == 0) sh.key1[n] = (uint32_t)total;
+    if (tid == 0 && !bmp) sh.key1[n] = (uint32_t)total;
     s6_sync();
     int32_t* zrel = reinterpret_cast<int32_t*>(g.pos);
     for (int l = tid + 1; l <= lrows; l += kS7Compute) zrel[l] = (int32_t)sh.key1[sh.ML[l]];
@@ -497,6 +672,7 @@ __global__ void __launch_bounds__(kS7Threads, S7Cfg<V, K>::MINB) spadd7_kernel(c
       mbar_init(&sh.full[s], 1);
       mbar_init(&sh.done[s], 1);
       mbar_init(&sh.empty[s], 1);
+      sh.excl_ok[s] = 0;
     }
     fence_barrier_init();
   }
