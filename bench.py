@@ -28,6 +28,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "GNNZ/s (3-way CSR SpAdd A+B+C on C2: partition + assembly + compute), % of HBM roofline"
+NOMINAL_HBM_GBS = 8000.0   # north_star's "about 8 TB/s" (the roofline is also reported against it)
 
 
 def parse():
@@ -143,6 +144,16 @@ def ev(torch):
 
 
 # ------------------------------------------------------------------ workloads
+def spadd_algo_bytes(ops, nnz_z):
+    """Algorithmic bytes of one k-way SpAdd: every operand's crd / val once, every
+    distinct row-pointer array once (C2's operands share one pos array), Z written once."""
+    vs = ops[0].val.element_size()
+    M = ops[0].nrows
+    pos_arrays = {A.pos.data_ptr() for A in ops}
+    return (sum(A.nnz * (4 + vs) for A in ops) + len(pos_arrays) * (M + 1) * 8
+            + nnz_z * (4 + vs) + (M + 1) * 8)
+
+
 def bench_spadd(N, W, torch, args, timer, world, rank):
     wl = W.build("c2", args.scale, device="cuda")
     ops = wl.ops
@@ -190,7 +201,7 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
             ex_ms.append(e0.elapsed_time(e1))
         nnz_z = int(zz[0][-1].item())
         vs = ops[0].val.element_size()
-        algo = (sum(n * (4 + vs) + (M + 1) * 8 for n in nnz) + nnz_z * (4 + vs) + (M + 1) * 8) / world
+        algo = spadd_algo_bytes(ops, nnz_z) / world
         return dict(work=qstar, times=times, sec=sec, launches=4, algo_step=algo, nnz_z=nnz_z, P=P,
                     kernel_bytes={"spadd_staged": algo, "partition_slice": (lparts.P + 1) * (8 * k + 28)},
                     two_pass={}, dtype="f32" if vs == 4 else "f64", wl=wl, parts=lparts,
@@ -289,8 +300,8 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
     times, sec = timer.run(step, args.steps, args.warmup, sections, soak_s=1.0)
     nnz_z = int(part_off[-1].item())
     vs = ops[0].val.element_size()
-    algo_step = sum(n * (4 + vs) + (M + 1) * 8 for n in nnz) + nnz_z * (4 + vs) + (M + 1) * 8
-    fused_bytes = sum(n * (4 + vs) + (M + 1) * 8 for n in nnz) + nnz_z * (4 + vs) + (M + 1) * 8
+    algo_step = spadd_algo_bytes(ops, nnz_z)
+    fused_bytes = algo_step
     res = dict(work=qstar / world if world > 1 else qstar, times=times, sec=sec, launches=launches,
                algo_step=algo_step, nnz_z=nnz_z, P=P,
                kernel_bytes={best: fused_bytes, "partition": (P + 1) * (8 * k + 28)},
@@ -460,20 +471,102 @@ def oracle_spadd_once(O, host_ops, P):
     return time.perf_counter() - t0
 
 
+def host_info():
+    """CPU model, logical CPUs and RAM of the machine the oracle runs on."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ram = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                ram = round(int(line.split()[1]) / 2 ** 20, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "ram_gib": ram}
+
+
+class pinned_core:
+    """Runs the single-threaded oracle pinned to one host core (SURVEY 8(d) 'Timing (oracle)')."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = min(self.old)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.old)
+
+
 def cpu_baseline(host_ops, P, budget_s=20.0):
     import oracle as O
     O.lib()
     qstar = sum(A.nnz for A in host_ops)
     ts = []
-    t_start = time.perf_counter()
-    while len(ts) < 3 or (time.perf_counter() - t_start < budget_s * 0.5 and len(ts) < 14):
-        ts.append(oracle_spadd_once(O, host_ops, P))
-        if time.perf_counter() - t_start > budget_s:
-            break
+    with pinned_core() as pc:
+        t_start = time.perf_counter()
+        while len(ts) < 3 or (time.perf_counter() - t_start < budget_s * 0.5 and len(ts) < 14):
+            ts.append(oracle_spadd_once(O, host_ops, P))
+            if time.perf_counter() - t_start > budget_s:
+                break
     med = statistics.median(ts)
-    return {"value": qstar / med / 1e9, "unit": "GNNZ/s", "cores": 1, "kind": "oracle",
+    return {"value": qstar / med / 1e9, "unit": "GNNZ/s", "cores": 1, "kind": "oracle", "pinned_core": pc.core,
+            "host": host_info(),
             "sample": f"full C2 workload (3 x {host_ops[0].nnz} nnz, P={P}): oracle partition_rank + spadd_k, "
-                      f"median of {len(ts)} runs on 1 host core, {med:.3f} s each"}
+                      f"median of {len(ts)} runs on 1 pinned host core, {med:.3f} s each"}
+
+
+def cpu_baseline_spmv(A, x, P, budget_s=20.0, max_rows=None):
+    """The oracle's SpMV (partition_rank + spmv) on a row-block sample of a large matrix (host RAM and
+    run time bound the sample; 'stream A in row blocks and time only the compute')."""
+    import oracle as O
+    import workloads as W
+    O.lib()
+    pos = A.pos.cpu().numpy()
+    M = A.nrows
+    # the first rows holding ~2e8 entries (the whole matrix when it is smaller)
+    target = min(int(pos[-1]), 200_000_000)
+    r1 = int(np.searchsorted(pos, target, side="left"))
+    r1 = max(1, min(M, r1 if max_rows is None else min(r1, max_rows)))
+    lo, hi = 0, int(pos[r1])
+    sub = W.SparseMatrix("csr", r1, A.ncols, pos[: r1 + 1] - lo, A.crd[lo:hi].cpu().numpy(),
+                         A.val[lo:hi].cpu().numpy())
+    xs = x.cpu().numpy()
+    ts = []
+    with pinned_core() as pc:
+        t_start = time.perf_counter()
+        while len(ts) < 3 and time.perf_counter() - t_start < budget_s:
+            t0 = time.perf_counter()
+            O.partition_rank([sub], max(1, P * (hi - lo) // max(1, int(pos[-1]))))
+            O.spmv(sub, xs)
+            ts.append(time.perf_counter() - t0)
+    med = statistics.median(ts)
+    return {"value": (hi - lo) / med / 1e9, "unit": "GNNZ/s", "cores": 1, "kind": "oracle", "pinned_core": pc.core,
+            "host": host_info(),
+            "sample": f"rows [0, {r1}) of the workload ({hi - lo} nnz of {int(pos[-1])}): oracle partition_rank + "
+                      f"spmv, median of {len(ts)} runs on 1 pinned host core, {med:.3f} s each"}
+
+
+def reference_partitions(host):
+    """P the library would choose (nacho_auto_partitions reads only the descriptors' sizes)."""
+    try:
+        import torch
+        import paper_2604_17198_b200 as N
+        import workloads as W
+        t = [W.SparseMatrix(A.format, A.nrows, A.ncols, torch.from_numpy(A.pos), torch.from_numpy(A.crd),
+                            torch.from_numpy(A.val)) for A in host]
+        return N.auto_partitions(t, "spadd")
+    except Exception:   # library not built: the same rule (tile entries minus the pad and Theorem 1 slack)
+        k = len(host)
+        tile = 2048 - 7 * k - (k - 1)
+        return max(1, -(-sum(A.nnz for A in host) // tile))
 
 
 def run_reference(args):
@@ -486,17 +579,19 @@ def run_reference(args):
     wl = W.build("c2", args.scale)
     host = wl.ops
     qstar = sum(A.nnz for A in host)
-    P = -(-qstar // 2046)
-    for _ in range(args.warmup):
-        oracle_spadd_once(O, host, P)
-    ts = [oracle_spadd_once(O, host, P) for _ in range(args.steps)]
+    P = reference_partitions(host)
+    with pinned_core() as pc:
+        for _ in range(args.warmup):
+            oracle_spadd_once(O, host, P)
+        ts = [oracle_spadd_once(O, host, P) for _ in range(args.steps)]
     ms = statistics.mean(ts) * 1e3
     v = qstar / (ms * 1e-3) / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GNNZ/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "c2_spadd3_1Mx1M_3x1e7nnz", "scale": args.scale},
-            "cpu_baseline": {"value": v, "unit": "GNNZ/s", "cores": 1, "kind": "oracle",
+            "config": {"workload": "c2_spadd3_1Mx1M_3x1e7nnz", "scale": args.scale, "P": P},
+            "cpu_baseline": {"value": v, "unit": "GNNZ/s", "cores": 1, "kind": "oracle", "pinned_core": pc.core,
+                             "host": host_info(),
                              "sample": f"full C2 workload each step ({qstar} nnz), oracle partition_rank + spadd_k"},
             "e2e": {"value": v, "unit": "GNNZ/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -556,7 +651,8 @@ def main():
                    **({"z_output": "sharded across ranks (device cut of Alg. 1); the all-gather of Z is timed "
                                    "separately as exchange_ms"} if world > 1 else {})},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": tt, "peak_source": peak_src,
+                     "frac": achieved / peak, "frac_nominal_8tbs": achieved / NOMINAL_HBM_GBS, "traffic": tt,
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": r["kernel_bytes"][dom]},
         "step_roofline_frac": summ["step_hbm_frac"],
         "sections_ms": summ["sections_ms"],
@@ -585,7 +681,7 @@ def main():
                 s, d, _, ach = summarize(rr, peak)
                 kern[name] = {"gnnz_s": s["gnnz_s"], "ms_per_step": s["ms_per_step"],
                               "step_hbm_frac": s["step_hbm_frac"], "dominant": d,
-                              "dominant_hbm_frac": ach / peak, "sections_ms": s["sections_ms"], "P": s["P"],
+                              "dominant_hbm_frac": ach / peak, "dominant_frac_nominal_8tbs": ach / NOMINAL_HBM_GBS, "sections_ms": s["sections_ms"], "P": s["P"],
                               "traffic": traffic_table().get(f"{name.split('_')[0]}:{d}")}
                 del rr
             except Exception as e:  # report, never hide
