@@ -33,7 +33,8 @@ typedef enum {
   NACHO_ERR_FORMAT = 3,      /* nacho_validate found a violated sorted-level invariant */
   NACHO_ERR_OVERFLOW = 4,    /* nrows or ncols > INT32_MAX, or a count does not fit the index types */
   NACHO_ERR_WORKSPACE = 5,   /* ws_bytes smaller than the *_workspace_size() result */
-  NACHO_ERR_CUDA = 6         /* a launch or CUDA runtime call failed */
+  NACHO_ERR_CUDA = 6,        /* a launch or CUDA runtime call failed */
+  NACHO_ERR_NCCL = 7         /* NCCL not loadable, or an NCCL call failed (multi-GPU calls only) */
 } nacho_status;
 
 typedef enum { NACHO_CSR = 0, NACHO_DCSR = 1 } nacho_format;
@@ -183,6 +184,70 @@ nacho_status nacho_spmm(const nacho_matrix* A, const nacho_parts* parts, const v
  * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.
  * Synchronous on `stream` (it reads one flag back).  Returns NACHO_ERR_FORMAT on a violation. */
 nacho_status nacho_validate(const nacho_matrix* A, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * Multi-GPU (one process per GPU).  The paper's partition is the device decomposition:
+ * with D devices, device d owns [b_d, b_{d+1}) of Alg. 1 run with P = D (one partition
+ * per processor; saved positions P:1795), so its work is Q* / D +- Delta (Theorem 1).  The
+ * paper is shared-memory only: the exchange below is this library's addition.  NCCL is
+ * loaded at run time (libnccl.so.2, the copy torch already loaded if any); failures -> NACHO_ERR_NCCL.
+ * torch (or any launcher) only moves the unique id between processes. */
+typedef struct nacho_dist_s nacho_dist;
+
+/* Size of the opaque NCCL unique id (bytes); nacho_dist_unique_id fills a HOST buffer of that size on
+ * one process, which hands it to every rank (e.g. a torch.distributed broadcast). */
+size_t nacho_dist_unique_id_size(void);
+nacho_status nacho_dist_unique_id(void* id);
+
+/* Communicator of `nranks` processes, this one `rank` (the current CUDA device is used).  Collective:
+ * every rank calls it.  Destroy with nacho_dist_destroy. */
+nacho_status nacho_dist_init(nacho_dist** comm, const void* id, int32_t nranks, int32_t rank);
+nacho_status nacho_dist_destroy(nacho_dist* comm);
+
+/* In-place broadcast of `bytes` of a device buffer from `root` (the x / B replication at setup). */
+nacho_status nacho_dist_broadcast(nacho_dist* comm, void* buf, size_t bytes, int32_t root, void* stream);
+
+/* Device cuts of one CSR operand for D devices: cuts[2d] = row, cuts[2d+1] = position of Alg. 1 at
+ * Q_d = floor(d Q* / D) (k = 1 closed form: position Q_d, row = highest x with pos[x] <= Q_d; cut 0 is
+ * the origin and cut D the end, R1).  `cuts`: device int64[2(D+1)].  Reads only A->pos. */
+nacho_status nacho_device_cuts(const nacho_matrix* A, int32_t D, int64_t* cuts, void* stream);
+
+/* Row pointers of a shard: rows [row_lo, row_lo + nloc) of `pos` restricted to positions
+ * [pos_lo, pos_hi) and rebased to 0 (first / last row possibly partial).  local_pos: device
+ * int64[nloc + 1].  A k-operand SpAdd shard calls it once per operand with that operand's cut
+ * positions b_d.pos[o], b_{d+1}.pos[o]. */
+nacho_status nacho_shard_rows(const int64_t* pos, int64_t row_lo, int64_t nloc, int64_t pos_lo, int64_t pos_hi,
+                              int64_t* local_pos, void* stream);
+
+/* Seam fix-up of device d (Listing 8's carry rule, at device level): if the device owns
+ * its first row (owns_first), add the carries of the devices before it that end in that row
+ * (carries: device int64[2D] of (row, value bits), row -1 = none), in device order, to y_local[0]. */
+nacho_status nacho_dist_seam(const int64_t* carries, int32_t D, int32_t d, int64_t row_lo, int32_t owns_first,
+                             int32_t dtype, void* y_local, void* stream);
+
+/* y = A x on D devices: this device's shard A_local (rows cut_rows[d] .. cut_rows[d+1] of A, the last
+ * one partial when d < D-1; nacho_device_cuts + nacho_shard_rows), its partitions `parts` (or NULL:
+ * auto P), the replicated x.  y_local[nrows_local] receives the rows the device owns (R7: rows
+ * [cut_rows[d], cut_rows[d+1]); its last slot is the outgoing seam carry when d < D-1), after the seam
+ * carries of earlier devices are added (an NCCL all-gather of one (row, value) pair per device).  If
+ * y_full (device, [nrows of A]) is not NULL every device's owned segment is gathered into it (one
+ * NCCL broadcast per device).  cut_rows: HOST int64[D+1] (cut D = nrows).  Collective. */
+size_t nacho_dist_spmv_workspace_size(const nacho_matrix* A_local, int32_t P, int32_t D);
+nacho_status nacho_dist_spmv(nacho_dist* comm, const nacho_matrix* A_local, const nacho_parts* parts, const void* x,
+                             void* y_local, const int64_t* cut_rows, void* y_full, void* ws, size_t ws_bytes,
+                             void* stream);
+
+/* Exchange step of a k-way SpAdd on D devices: every device has run nacho_spadd_k on its operand
+ * shards (rows cut_rows[d] .. cut_rows[d+1]); z_*_local is its union and nnz_local (device int64[1])
+ * its size.  Equal coordinates never straddle a cut, so no values merge: an NCCL
+ * all-gather of the D sizes gives the global offsets (the host reads them: variable-size collectives
+ * need host counts -- the call synchronises `stream`), then Z.crd / Z.val / Z.pos segments are
+ * gathered into z_pos[nrows+1] / z_crd / z_val (capacity >= the total, returned in *nnz_total). */
+size_t nacho_dist_spadd_workspace_size(int32_t D);
+nacho_status nacho_dist_spadd_gather(nacho_dist* comm, const int64_t* z_pos_local, const int32_t* z_crd_local,
+                                     const void* z_val_local, int32_t dtype, const int64_t* nnz_local,
+                                     const int64_t* cut_rows, int64_t* z_pos, int32_t* z_crd, void* z_val,
+                                     int64_t* nnz_total, void* ws, size_t ws_bytes, void* stream);
 
 /* Message for the last non-success status on this thread ("" if none). */
 const char* nacho_last_error(void);

@@ -20,7 +20,8 @@ LIB_PATH = os.environ.get("NACHO_LIB", os.path.join(HERE, "libnacho.so"))
 NACHO_CSR, NACHO_DCSR = 0, 1
 NACHO_F32, NACHO_F64 = 0, 1
 MAX_K = 8
-STATUS = {0: "SUCCESS", 1: "INVALID_ARG", 2: "SHAPE", 3: "FORMAT", 4: "OVERFLOW", 5: "WORKSPACE", 6: "CUDA"}
+STATUS = {0: "SUCCESS", 1: "INVALID_ARG", 2: "SHAPE", 3: "FORMAT", 4: "OVERFLOW", 5: "WORKSPACE", 6: "CUDA",
+          7: "NCCL"}
 
 
 class NachoError(RuntimeError):
@@ -69,6 +70,21 @@ def _load():
     L.nacho_last_error.restype = ctypes.c_char_p
     L.nacho_launch_count.argtypes = [i32]
     L.nacho_launch_count.restype = i64
+    # multi-GPU (dist.cuh)
+    L.nacho_dist_unique_id_size.restype = sz
+    L.nacho_dist_unique_id.argtypes = [vp]
+    L.nacho_dist_init.argtypes = [ctypes.POINTER(vp), vp, i32, i32]
+    L.nacho_dist_destroy.argtypes = [vp]
+    L.nacho_dist_broadcast.argtypes = [vp, vp, sz, i32, vp]
+    L.nacho_device_cuts.argtypes = [vp, i32, vp, vp]
+    L.nacho_shard_rows.argtypes = [vp, i64, i64, i64, i64, vp, vp]
+    L.nacho_dist_seam.argtypes = [vp, i32, i32, i64, i32, i32, vp, vp]
+    L.nacho_dist_spmv_workspace_size.argtypes = [vp, i32, i32]
+    L.nacho_dist_spmv_workspace_size.restype = sz
+    L.nacho_dist_spmv.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_dist_spadd_workspace_size.argtypes = [i32]
+    L.nacho_dist_spadd_workspace_size.restype = sz
+    L.nacho_dist_spadd_gather.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, ctypes.POINTER(i64), vp, sz, vp]
     return L
 
 
@@ -78,7 +94,10 @@ EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", 
            "nacho_spadd_k_workspace_size", "nacho_spadd_k_count", "nacho_spadd_k_fill", "nacho_spadd_k",
            "nacho_spadd_k_staged_workspace_size", "nacho_spadd_k_staged",
            "nacho_spmm_workspace_size", "nacho_spmm", "nacho_validate", "nacho_last_error",
-           "nacho_launch_count"]
+           "nacho_launch_count", "nacho_dist_unique_id_size", "nacho_dist_unique_id", "nacho_dist_init",
+           "nacho_dist_destroy", "nacho_dist_broadcast", "nacho_device_cuts", "nacho_shard_rows", "nacho_dist_seam",
+           "nacho_dist_spmv_workspace_size", "nacho_dist_spmv", "nacho_dist_spadd_workspace_size",
+           "nacho_dist_spadd_gather"]
 
 
 def _check(status):
@@ -304,3 +323,101 @@ def validate(A, stream=None):
 
 def launch_count(reset: bool = False) -> int:
     return lib.nacho_launch_count(int(reset))
+
+
+# ------------------------------------------------------------------ multi-GPU (include/nacho.h, dist.cuh)
+def device_cuts(A, D: int, stream=None) -> torch.Tensor:
+    """nacho_device_cuts: the D+1 device cuts (row, position) of Alg. 1 with P = D on one CSR operand
+    (reads only A.pos).  Returns a device int64 tensor [D+1, 2]."""
+    cuts = torch.empty((D + 1, 2), dtype=torch.int64, device=A.pos.device)
+    m = matrix_pos_only(A)
+    _check(lib.nacho_device_cuts(ctypes.byref(m), D, _ptr(cuts), _stream(stream)))
+    return cuts
+
+
+def matrix_pos_only(A) -> Matrix:
+    """Descriptor of an operand of which only pos (and the sizes) are resident (device cuts)."""
+    _require(A.pos, torch.int64, "pos")
+    m = Matrix()
+    m.format, m.dtype = NACHO_CSR, NACHO_F32
+    m.nrows, m.ncols = int(A.nrows), int(A.ncols)
+    m.nouter = int(A.pos.shape[0]) - 1
+    m.nnz = int(A.nnz)
+    m.pos = A.pos.data_ptr()
+    return m
+
+
+def shard_rows(pos: torch.Tensor, row_lo: int, nloc: int, pos_lo: int, pos_hi: int, stream=None) -> torch.Tensor:
+    """nacho_shard_rows: rebased row pointers of rows [row_lo, row_lo + nloc) within [pos_lo, pos_hi)."""
+    out = torch.empty(nloc + 1, dtype=torch.int64, device=pos.device)
+    _check(lib.nacho_shard_rows(_ptr(pos), row_lo, nloc, pos_lo, pos_hi, _ptr(out), _stream(stream)))
+    return out
+
+
+def dist_seam(carries: torch.Tensor, D: int, d: int, row_lo: int, owns_first: bool, y_local: torch.Tensor, stream=None):
+    """nacho_dist_seam: add the seam carries of devices < d ending in row_lo to y_local[0]."""
+    dt = NACHO_F64 if y_local.dtype == torch.float64 else NACHO_F32
+    _check(lib.nacho_dist_seam(_ptr(carries), D, d, row_lo, int(bool(owns_first)), dt, _ptr(y_local), _stream(stream)))
+
+
+class Dist:
+    """nacho_dist communicator (NCCL inside libnacho.so).  torch.distributed only moves the unique id."""
+
+    def __init__(self, nranks: int, rank: int, id_bytes: bytes):
+        self.nranks, self.rank = nranks, rank
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(id_bytes, len(id_bytes))
+        _check(lib.nacho_dist_init(ctypes.byref(h), buf, nranks, rank))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        n = lib.nacho_dist_unique_id_size()
+        buf = ctypes.create_string_buffer(n)
+        _check(lib.nacho_dist_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls):
+        """Rank 0 creates the NCCL unique id; a torch.distributed broadcast hands it to every rank."""
+        import torch.distributed as td
+        n = lib.nacho_dist_unique_id_size()
+        obj = [cls.unique_id() if td.get_rank() == 0 else None]
+        td.broadcast_object_list(obj, src=0)
+        assert len(obj[0]) == n
+        return cls(td.get_world_size(), td.get_rank(), obj[0])
+
+    def broadcast(self, t: torch.Tensor, root: int = 0, stream=None):
+        _check(lib.nacho_dist_broadcast(self.h, _ptr(t), t.numel() * t.element_size(), root, _stream(stream)))
+
+    def spmv(self, A_local, parts, x, y_local, cut_rows, y_full=None, ws=None, stream=None):
+        """nacho_dist_spmv: local partitions + seam carries (+ gather of the owned y segments)."""
+        m = matrix(A_local)
+        P = parts.P if parts is not None else 0
+        need = lib.nacho_dist_spmv_workspace_size(ctypes.byref(m), P, self.nranks)
+        if ws is None or ws.numel() < need:
+            ws, _ = _workspace(need, x.device)
+        cr = (ctypes.c_int64 * (self.nranks + 1))(*[int(c) for c in cut_rows])
+        pc = ctypes.byref(parts.c()) if parts is not None else None
+        _check(lib.nacho_dist_spmv(self.h, ctypes.byref(m), pc, _ptr(x), _ptr(y_local), cr, _ptr(y_full), _ptr(ws),
+                                   need, _stream(stream)))
+        return y_local
+
+    def spadd_gather(self, z_pos_local, z_crd_local, z_val_local, nnz_local, cut_rows, z_pos, z_crd, z_val, ws=None,
+                     stream=None):
+        """nacho_dist_spadd_gather: global offsets from the device union sizes, Z segments gathered."""
+        need = lib.nacho_dist_spadd_workspace_size(self.nranks)
+        if ws is None or ws.numel() < need:
+            ws, _ = _workspace(need, z_pos.device)
+        cr = (ctypes.c_int64 * (self.nranks + 1))(*[int(c) for c in cut_rows])
+        tot = ctypes.c_int64(0)
+        dt = NACHO_F64 if z_val_local.dtype == torch.float64 else NACHO_F32
+        _check(lib.nacho_dist_spadd_gather(self.h, _ptr(z_pos_local), _ptr(z_crd_local), _ptr(z_val_local), dt,
+                                           _ptr(nnz_local), cr, _ptr(z_pos), _ptr(z_crd), _ptr(z_val),
+                                           ctypes.byref(tot), _ptr(ws), need, _stream(stream)))
+        return int(tot.value)
+
+    def close(self):
+        if self.h:
+            _check(lib.nacho_dist_destroy(self.h))
+            self.h = None

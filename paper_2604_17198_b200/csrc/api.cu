@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "partition.cuh"
@@ -15,6 +16,7 @@
 #include "spadd5.cuh"
 #include "spadd6.cuh"
 #include "spadd7.cuh"
+#include "dist.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
 #include "spmv3.cuh"
@@ -552,6 +554,186 @@ int spadd_impl() {
 }  // namespace
 
 extern "C" {
+
+/* ------------------------------------------------------------------ multi-GPU (dist.cuh) */
+#define NACHO_NCCL(call)                                                                              \
+  do {                                                                                                \
+    const ncclResult_t _r = (call);                                                                   \
+    if (_r != ncclSuccess) return fail(NACHO_ERR_NCCL, "%s: %s", #call, nccl().GetErrorString(_r));  \
+  } while (0)
+
+size_t nacho_dist_unique_id_size(void) { return sizeof(ncclUniqueId); }
+
+nacho_status nacho_dist_unique_id(void* id) {
+  if (!id) return fail(NACHO_ERR_INVALID_ARG, "null id buffer");
+  if (!nccl().ok) return fail(NACHO_ERR_NCCL, "libnccl.so.2 not loadable");
+  NACHO_NCCL(nccl().GetUniqueId(static_cast<ncclUniqueId*>(id)));
+  return NACHO_SUCCESS;
+}
+
+nacho_status nacho_dist_init(nacho_dist** comm, const void* id, int32_t nranks, int32_t rank) {
+  if (!comm || !id) return fail(NACHO_ERR_INVALID_ARG, "null comm / id");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NACHO_ERR_INVALID_ARG, "rank %d of %d", rank, nranks);
+  if (!nccl().ok) return fail(NACHO_ERR_NCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c;
+  NACHO_NCCL(nccl().CommInitRank(&c, nranks, uid, rank));
+  *comm = new nacho_dist_s{c, nranks, rank};
+  return NACHO_SUCCESS;
+}
+
+nacho_status nacho_dist_destroy(nacho_dist* comm) {
+  if (!comm) return NACHO_SUCCESS;
+  const ncclResult_t r = nccl().CommDestroy(comm->comm);
+  delete comm;
+  if (r != ncclSuccess) return fail(NACHO_ERR_NCCL, "ncclCommDestroy: %s", nccl().GetErrorString(r));
+  return NACHO_SUCCESS;
+}
+
+nacho_status nacho_dist_broadcast(nacho_dist* comm, void* buf, size_t bytes, int32_t root, void* stream) {
+  if (!comm || (!buf && bytes)) return fail(NACHO_ERR_INVALID_ARG, "null comm / buffer");
+  if (root < 0 || root >= comm->nranks) return fail(NACHO_ERR_INVALID_ARG, "root %d", root);
+  NACHO_NCCL(nccl().Broadcast(buf, buf, bytes, ncclChar, root, comm->comm, static_cast<cudaStream_t>(stream)));
+  return NACHO_SUCCESS;
+}
+
+nacho_status nacho_device_cuts(const nacho_matrix* A, int32_t D, int64_t* cuts, void* stream) {
+  if (!A || !A->pos) return fail(NACHO_ERR_INVALID_ARG, "A: null descriptor / pos");   // crd / val not read
+  if (A->format != NACHO_CSR || A->nouter < 0 || A->nnz < 0) return fail(NACHO_ERR_INVALID_ARG, "A: CSR sizes");
+  if (D < 1 || !cuts) return fail(NACHO_ERR_INVALID_ARG, "D = %d / null cuts", D);
+  device_cuts_kernel<<<(D + 1 + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(A->pos, A->nouter, A->nnz, D,
+                                                                                          cuts);
+  return launched("device_cuts_kernel");
+}
+
+nacho_status nacho_shard_rows(const int64_t* pos, int64_t row_lo, int64_t nloc, int64_t pos_lo, int64_t pos_hi,
+                              int64_t* local_pos, void* stream) {
+  if (!pos || !local_pos) return fail(NACHO_ERR_INVALID_ARG, "null pos / local_pos");
+  if (row_lo < 0 || nloc < 0 || pos_lo < 0 || pos_hi < pos_lo) return fail(NACHO_ERR_INVALID_ARG, "bad shard range");
+  const int64_t g = std::min<int64_t>((nloc + 256) / 256, 148 * 16);
+  shard_rows_kernel<<<(unsigned)std::max<int64_t>(g, 1), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      pos, row_lo, nloc, pos_lo, pos_hi, local_pos);
+  return launched("shard_rows_kernel");
+}
+
+nacho_status nacho_dist_seam(const int64_t* carries, int32_t D, int32_t d, int64_t row_lo, int32_t owns_first,
+                             int32_t dtype, void* y_local, void* stream) {
+  if (!carries || !y_local) return fail(NACHO_ERR_INVALID_ARG, "null carries / y_local");
+  if (D < 1 || d < 0 || d >= D) return fail(NACHO_ERR_INVALID_ARG, "device %d of %d", d, D);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == NACHO_F64) seam_kernel<double><<<1, 32, 0, st>>>(carries, D, d, row_lo, owns_first, static_cast<double*>(y_local));
+  else seam_kernel<float><<<1, 32, 0, st>>>(carries, D, d, row_lo, owns_first, static_cast<float*>(y_local));
+  return launched("seam_kernel");
+}
+
+size_t nacho_dist_spmv_workspace_size(const nacho_matrix* A_local, int32_t P, int32_t D) {
+  return nacho_spmv_workspace_size(A_local, P) + align_up(2 * 8) + align_up((size_t)(D > 0 ? D : 1) * 2 * 8);
+}
+
+nacho_status nacho_dist_spmv(nacho_dist* comm, const nacho_matrix* A_local, const nacho_parts* parts, const void* x,
+                             void* y_local, const int64_t* cut_rows, void* y_full, void* ws, size_t ws_bytes,
+                             void* stream) {
+  if (!comm || !cut_rows) return fail(NACHO_ERR_INVALID_ARG, "null comm / cut_rows");
+  NACHO_TRY(check_matrix(A_local, "A_local"));
+  if (A_local->format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "dist SpMV shards CSR operands");
+  const int D = comm->nranks, d = comm->rank;
+  const size_t need = nacho_dist_spmv_workspace_size(A_local, parts ? parts->P : 0, D);
+  if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  const size_t sw = nacho_spmv_workspace_size(A_local, parts ? parts->P : 0);
+  char* w = static_cast<char*>(ws);
+  int64_t* send = reinterpret_cast<int64_t*>(w + sw);
+  int64_t* carries = reinterpret_cast<int64_t*>(w + sw + align_up(2 * 8));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t nloc = A_local->nrows;
+  const int64_t row_lo = cut_rows[d];
+  const int64_t own = cut_rows[d + 1] - row_lo;   // rows this device owns (R7)
+  // + the row cut by b_{d+1} (its seam carry), unless the cut is the end of the rows
+  const bool has_carry = d < D - 1 && cut_rows[d + 1] < cut_rows[D];
+  const int64_t expect = own + (has_carry ? 1 : 0);
+  if (nloc != expect)
+    return fail(NACHO_ERR_SHAPE, "shard holds %lld rows, the cut %lld", (long long)nloc, (long long)expect);
+  // 1. the device's partitions (P:1089-1093 on the shard)
+  NACHO_TRY(nacho_spmv(A_local, parts, x, y_local, 0, w, sw, stream));
+  // 2. seam carries: all-gather of (row, partial) pairs, added in device order by the owner
+  const bool f64 = A_local->dtype == NACHO_F64;
+  if (f64) carry_pack_kernel<double><<<1, 32, 0, st>>>(static_cast<double*>(y_local), nloc, row_lo, has_carry, send);
+  else carry_pack_kernel<float><<<1, 32, 0, st>>>(static_cast<float*>(y_local), nloc, row_lo, has_carry, send);
+  NACHO_TRY(launched("carry_pack_kernel"));
+  NACHO_NCCL(nccl().AllGather(send, carries, 2, ncclInt64, comm->comm, st));
+  NACHO_TRY(nacho_dist_seam(carries, D, d, row_lo, own > 0, A_local->dtype, y_local, stream));
+  // 3. optional gather of the owned y segments (one broadcast per device, grouped)
+  if (y_full) {
+    const size_t es = f64 ? 8 : 4;
+    NACHO_NCCL(nccl().GroupStart());
+    for (int r = 0; r < D; ++r) {
+      const int64_t own_r = cut_rows[r + 1] - cut_rows[r];
+      if (own_r <= 0) continue;
+      void* dst = static_cast<char*>(y_full) + (size_t)cut_rows[r] * es;
+      NACHO_NCCL(nccl().Broadcast(r == d ? y_local : dst, dst, (size_t)own_r, f64 ? ncclFloat64 : ncclFloat32, r,
+                                  comm->comm, st));
+    }
+    NACHO_NCCL(nccl().GroupEnd());
+  }
+  return NACHO_SUCCESS;
+}
+
+size_t nacho_dist_spadd_workspace_size(int32_t D) {
+  const size_t De = D > 0 ? D : 1;
+  return align_up(8) + align_up(De * 8) + align_up((De + 1) * 8);
+}
+
+nacho_status nacho_dist_spadd_gather(nacho_dist* comm, const int64_t* z_pos_local, const int32_t* z_crd_local,
+                                     const void* z_val_local, int32_t dtype, const int64_t* nnz_local,
+                                     const int64_t* cut_rows, int64_t* z_pos, int32_t* z_crd, void* z_val,
+                                     int64_t* nnz_total, void* ws, size_t ws_bytes, void* stream) {
+  if (!comm || !cut_rows || !z_pos_local || !nnz_local || !z_pos) return fail(NACHO_ERR_INVALID_ARG, "null argument");
+  const int D = comm->nranks, d = comm->rank;
+  const size_t need = nacho_dist_spadd_workspace_size(D);
+  if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  char* w = static_cast<char*>(ws);
+  int64_t* counts = reinterpret_cast<int64_t*>(w + align_up(8));
+  int64_t* off = reinterpret_cast<int64_t*>(w + align_up(8) + align_up((size_t)D * 8));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // 1. device union sizes -> global offsets (P:1475 at device level)
+  NACHO_NCCL(nccl().AllGather(nnz_local, counts, 1, ncclInt64, comm->comm, st));
+  offsets_kernel<<<1, 32, 0, st>>>(counts, D, off);
+  NACHO_TRY(launched("offsets_kernel"));
+  std::vector<int64_t> h(D + 1);
+  if (cudaMemcpyAsync(h.data(), off, (D + 1) * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)   // variable-size collectives need the counts on the host
+    return fail(NACHO_ERR_CUDA, "reading the device offsets");
+  if (nnz_total) *nnz_total = h[D];
+  if ((!z_crd || !z_val) && h[D] > 0) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
+  // 2. this device's Z.pos rows (row_lo, row_hi] at its offset, then every segment gathered
+  const int64_t M = cut_rows[D];
+  const int64_t own = (d < D - 1 ? cut_rows[d + 1] : M) - cut_rows[d];
+  if (own > 0) {
+    zpos_segment_kernel<<<(unsigned)std::min<int64_t>((own + 255) / 256, 148 * 16), 256, 0, st>>>(
+        z_pos_local, own, off + d, z_pos + cut_rows[d] + 1);
+    NACHO_TRY(launched("zpos_segment_kernel"));
+  }
+  if (d == 0 && cudaMemsetAsync(z_pos, 0, 8, st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "z_pos[0]");
+  const size_t es = dtype == NACHO_F64 ? 8 : 4;
+  NACHO_NCCL(nccl().GroupStart());
+  for (int r = 0; r < D; ++r) {
+    const int64_t own_r = (r < D - 1 ? cut_rows[r + 1] : M) - cut_rows[r];
+    const int64_t cnt = h[r + 1] - h[r];
+    if (cnt > 0) {
+      NACHO_NCCL(nccl().Broadcast(r == d ? (const void*)z_crd_local : z_crd + h[r], z_crd + h[r], (size_t)cnt, ncclInt32, r,
+                                  comm->comm, st));
+      void* vdst = static_cast<char*>(z_val) + (size_t)h[r] * es;
+      NACHO_NCCL(nccl().Broadcast(r == d ? z_val_local : vdst, vdst, (size_t)cnt, es == 8 ? ncclFloat64 : ncclFloat32,
+                                  r, comm->comm, st));
+    }
+    if (own_r > 0)
+      NACHO_NCCL(nccl().Broadcast(z_pos + cut_rows[r] + 1, z_pos + cut_rows[r] + 1, (size_t)own_r, ncclInt64, r,
+                                  comm->comm, st));
+  }
+  NACHO_NCCL(nccl().GroupEnd());
+  if (D > 1) NACHO_NCCL(nccl().Broadcast(z_pos, z_pos, 1, ncclInt64, 0, comm->comm, st));
+  return NACHO_SUCCESS;
+}
 
 const char* nacho_last_error(void) { return g_err.c_str(); }
 

@@ -1,9 +1,11 @@
-"""Multi-rank host logic of paper_2604_17198_b200.dist on CPU: world_size 2 (and 3) over gloo.
+"""Multi-GPU host logic on CPU: the shard plan the device cuts give, and the NCCL
+unique-id handoff of nacho_dist_init over a world-size-2 gloo group.
 
-The per-rank local results are emulated from the definition of what a rank's kernels produce for its
-slice of partitions (owned rows exact on the slice, one seam carry; the union of the slice's coordinate
-range); the exchange and assembly code under test is the one the NCCL path runs.  The assembled y / Z
-must equal the oracle's full result (I9: device cuts are a subset of the fine cuts)."""
+The device cuts are Alg. 1 with P = D; the plan must tile the rows exactly once (R7
+ownership), hold every position exactly once, and leave one seam row per device whose row continues
+on the next one (a dense row may span several devices).  The cuts are taken from the ORACLE here
+(partition_rank with P = D), so the plan logic is checked against the paper's definition; the GPU
+tests check nacho_device_cuts against the same oracle and run the kernels on the shards."""
 import os
 import socket
 
@@ -14,9 +16,64 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle as O
-import workloads as W
 from paper_2604_17198_b200 import dist as D
 from tests.util import random_csr
+
+
+def _oracle_cuts(A, ndev):
+    p = O.partition_rank([A], ndev)
+    return [(int(p.row_pos[d]), int(p.pos[d])) for d in range(ndev + 1)]
+
+
+def _check_plans(A, ndev):
+    plans = D.shard_plans(_oracle_cuts(A, ndev), A.nrows)
+    M = A.nrows
+    owned = np.zeros(M, np.int64)
+    held = 0
+    for p in plans:
+        owned[p.row_lo:p.row_lo + p.own] += 1
+        held += p.pos_hi - p.pos_lo
+        assert p.pos_lo <= p.pos_hi
+        # every held position lies in the held rows
+        if p.pos_hi > p.pos_lo:
+            r_first = int(np.searchsorted(A.pos, p.pos_lo, side="right") - 1)
+            r_last = int(np.searchsorted(A.pos, p.pos_hi - 1, side="right") - 1)
+            assert p.row_lo <= r_first and r_last < p.row_lo + max(p.nloc, 1)
+        # the seam row is the row the next device starts in
+        if p.has_carry:
+            assert p.row_lo + p.nloc - 1 == plans[p.d + 1].row_lo
+    assert (owned == 1).all(), "rows owned exactly once (R7)"
+    assert held == A.nnz, "positions held exactly once"
+    # work balance (Theorem 1 with Delta = 1 for one operand): floor / ceil of nnz / D
+    w = [p.pos_hi - p.pos_lo for p in plans]
+    assert max(w) - min(w) <= 1
+    return plans
+
+
+@pytest.mark.parametrize("ndev", [1, 2, 3, 8])
+def test_shard_plans_tile_rows_and_positions(ndev):
+    rng = np.random.default_rng(10 + ndev)
+    for trial in range(6):
+        M, N = int(rng.integers(5, 80)), int(rng.integers(5, 90))
+        A = random_csr(rng, M, N, float(rng.uniform(0.02, 0.3)), dense_rows=[int(rng.integers(M))] if trial % 2 else ())
+        _check_plans(A, ndev)
+
+
+def test_dense_row_spans_devices():
+    """A dense row longer than a device share: the devices inside it own no rows and pass carries on."""
+    rng = np.random.default_rng(3)
+    A = random_csr(rng, 12, 400, 0.01, dense_rows=[5], empty_frac=0.0)
+    plans = _check_plans(A, 8)
+    inside = [p for p in plans if p.own == 0]
+    assert inside, "some device lies entirely inside the dense row"
+    assert all(p.row_lo == 5 and p.has_carry for p in inside)
+
+
+def test_more_devices_than_entries():
+    A = random_csr(np.random.default_rng(1), 6, 6, 0.0, empty_frac=1.0)   # nnz = 0
+    plans = D.shard_plans(_oracle_cuts(A, 4), A.nrows)
+    assert plans[0].own == 6 and all(p.own == 0 and p.nloc == 0 for p in plans[1:])
+    assert D.cut_rows(plans, 6) == [0, 6, 6, 6, 6]
 
 
 def _free_port():
@@ -27,91 +84,33 @@ def _free_port():
     return p
 
 
-def _emulated_spmv_local(A, x, parts, lo, hi):
-    """What the kernels leave in a zeroed y for partitions [lo, hi) of a one-operand partition."""
-    s, e = int(parts.pos[lo]), int(parts.pos[hi])
-    own_lo, own_hi, seam = D.spmv_rank_rows(torch.from_numpy(parts.row_pos), lo, hi, A.nouter)
-    y = np.zeros(A.nouter, dtype=np.float64)
-    rows = list(range(own_lo, own_hi)) + ([seam] if seam >= 0 else [])
-    for r in rows:
-        a, b = max(int(A.pos[r]), s), min(int(A.pos[r + 1]), e)
-        y[r] = sum(float(A.val[q]) * float(x[A.crd[q]]) for q in range(a, b))
-    return torch.from_numpy(y), own_lo, own_hi, seam
-
-
-def _emulated_spadd_local(ops, parts, lo, hi, z):
-    """The union of the coordinate range [b_lo, b_hi) with local row pointers on the owned rows."""
-    z_pos, z_crd, z_val = z
-    M = ops[0].nrows
-    rows = np.repeat(np.arange(M), np.diff(z_pos))
-    keys = list(zip(rows.tolist(), z_crd.tolist()))
-    b_lo = (int(parts.row[lo]), int(parts.col[lo]))
-    b_hi = (int(parts.row[hi]), int(parts.col[hi]))
-    sel = np.array([b_lo <= kk < b_hi for kk in keys], dtype=bool) if keys else np.zeros(0, bool)
-    l_crd, l_val, l_rows = z_crd[sel], z_val[sel], rows[sel]
-    own_lo, own_hi = int(parts.row[lo]), int(parts.row[hi])
-    lp = np.zeros(M + 1, np.int64)
-    for r in range(own_lo, own_hi):
-        lp[r + 1] = int((l_rows <= r).sum())
-    return (torch.from_numpy(lp), torch.from_numpy(l_crd.astype(np.int32)), torch.from_numpy(l_val),
-            int(sel.sum()), own_lo, own_hi)
-
-
-def _worker(rank, world, port, seed, q):
+def _id_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        rng = np.random.default_rng(seed)
-        # ---- SpMV with a dense row that straddles the device cuts
-        A = random_csr(rng, 40, 60, 0.15, dtype=np.float64, dense_rows=[17], empty_frac=0.3)
-        x = rng.uniform(0.5, 1.5, 60)
-        P_total = 4 * world
-        parts = O.partition_rank([A], P_total)
-        lo, hi = D.rank_range(P_total, world, rank)
-        y_local, own_lo, own_hi, seam = _emulated_spmv_local(A, x, parts, lo, hi)
-        y = D.spmv_assemble(y_local, own_lo, own_hi, seam, A.nouter).numpy()
-        ref = O.spmv(A, x)
-        ok_spmv = np.allclose(y, ref, rtol=1e-12, atol=1e-12)
-        # ---- 3-way SpAdd: exact structure and values
-        base = random_csr(rng, 30, 50, 0.2, dtype=np.float32)
-        ops = [base] + [random_csr(rng, 30, 50, 0.1, dtype=np.float32, base=base, share=0.5) for _ in range(2)]
-        parts3 = O.partition_rank(ops, P_total)
-        z = O.spadd_k(ops)
-        lp, lc, lv, nl, olo, ohi = _emulated_spadd_local(ops, parts3, lo, hi, z)
-        zp, zc, zv = D.spadd_assemble(ops[0].nrows, lp, lc, lv, nl, olo, ohi)
-        ok_spadd = (np.array_equal(zp.numpy(), z[0]) and np.array_equal(zc.numpy(), z[1])
-                    and np.array_equal(zv.numpy(), z[2]))
-        q.put((rank, bool(ok_spmv), bool(ok_spadd)))
+        import paper_2604_17198_b200 as N
+        obj = [N.Dist.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        q.put((rank, obj[0]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,seed", [(2, 1), (2, 2), (3, 3)])
-def test_distributed_assembly_gloo(world, seed):
+def test_unique_id_handoff_gloo():
+    """nacho_dist_unique_id on rank 0, handed to every rank by torch.distributed (the only role torch
+    has in the multi-GPU path): every rank receives the same NACHO_DIST_UNIQUE_ID_SIZE bytes."""
+    import paper_2604_17198_b200 as N
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, q)) for r in range(world)]
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
+    res = dict(q.get(timeout=120) for _ in range(2))
     for p in procs:
         p.join(timeout=60)
-    assert all(r[1] for r in res), f"SpMV assembly mismatch: {res}"
-    assert all(r[2] for r in res), f"SpAdd assembly mismatch: {res}"
-
-
-def test_device_cuts_are_fine_cuts():
-    """I9: the device cuts of P = D are boundaries of P = D * P_l (floor(d*P_l*Q/(D*P_l)) = floor(d*Q/D))."""
-    rng = np.random.default_rng(4)
-    base = random_csr(rng, 50, 80, 0.2)
-    ops = [base, random_csr(rng, 50, 80, 0.1, base=base, share=0.5)]
-    for Dn, Pl in [(2, 3), (4, 5), (8, 2)]:
-        coarse = O.partition_rank(ops, Dn)
-        fine = O.partition_rank(ops, Dn * Pl)
-        assert np.array_equal(coarse.pos2(), fine.pos2()[::Pl])
-        assert np.array_equal(coarse.row, fine.row[::Pl]) and np.array_equal(coarse.col, fine.col[::Pl])
+    assert res[0] == res[1] and len(res[0]) == N.lib.nacho_dist_unique_id_size()
 
 
 def test_slice_parts_views_share_storage():

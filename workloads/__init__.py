@@ -242,6 +242,8 @@ def _lib():
         L.wl_columns_rows.argtypes = [ci, i64, i64, u64, vp, vp, i64, i64, u64, vp, vp]
         L.wl_values.argtypes = [u64, u64, i64, ci, ci, ci, vp, vp]
         L.wl_outer.argtypes = [i64, i64, u64, vp, vp]
+        L.wl_columns_range.argtypes = [ci, ci, i64, i64, u64, vp, i64, i64, u64, u64, u64, vp, vp]
+        L.wl_values_range.argtypes = [u64, u64, i64, i64, ci, ci, ci, vp, vp]
         _LIB = L
     return _LIB
 
@@ -310,3 +312,33 @@ class _DeviceGen:
         v = t.empty(n * nb, dtype=self.tdtype, device=self.device)
         self._chk(_lib().wl_values(self.cfg["seed"], stream, n * nb, 0, 4, int(self.f64), v.data_ptr(), self.stream))
         return v if nb == 1 else v.view(n, nb)
+
+
+# ------------------------------------------------------------------ device shards (multi-GPU setup)
+def full_pos(name: str, scale: float = 1.0, device: str = "cuda"):
+    """The full row-pointer array of a one-operand configuration (cheap: degrees only)."""
+    cfg = scaled(CONFIGS[name], scale)
+    gen = _DeviceGen(cfg, "uniform", 4, device)
+    return gen.pos(cfg["m"], cfg["target"], cap=cfg["m"], dense_row=cfg.get("dense_row")), cfg
+
+
+def shard_entries(name: str, pos, e_lo: int, e_hi: int, scale: float = 1.0, device: str = "cuda"):
+    """crd / val of entries [e_lo, e_hi) of configuration `name` -- bit-identical to the slice of the
+    full matrix build() makes (counter-based generator), so a device holds only its shard."""
+    import torch
+    cfg = scaled(CONFIGS[name], scale)
+    gen = _DeviceGen(cfg, "uniform", 4, device)
+    n = e_hi - e_lo
+    crd = torch.empty(n, dtype=torch.int32, device=gen.device)
+    m = cfg["m"]
+    gen._chk(_lib().wl_columns_range(KIND_ID[cfg["cols"]], 0, m, m, cfg["seed"], pos.data_ptr(), e_lo, e_hi,
+                                     STREAM_OP[0], STREAM_OP[0], STREAM_OP[1], crd.data_ptr(), gen.stream))
+    val = torch.empty(n, dtype=gen.tdtype, device=gen.device)
+    gen._chk(_lib().wl_values_range(cfg["seed"], 1000, e_lo, n, 0, 4, int(gen.f64), val.data_ptr(), gen.stream))
+    return crd, val
+
+
+def dense_x(name: str, scale: float = 1.0, device: str = "cuda"):
+    cfg = scaled(CONFIGS[name], scale)
+    gen = _DeviceGen(cfg, "uniform", 4, device)
+    return gen.dense(R.S_X, cfg["m"], 1)

@@ -93,9 +93,9 @@ __device__ __forceinline__ int64_t row_of_entry(const int64_t* __restrict__ pos,
 
 // mode: 0 plain (stream_own), 1 C2 operand B (reuse A 30%), 2 C2 operand C (reuse A or B 30%)
 __global__ void k_columns(int kind, int mode, int64_t m, int64_t n, uint64_t seed, const int64_t* __restrict__ pos,
-                          int64_t nnz, uint64_t stream_own, uint64_t stream_a, uint64_t stream_b,
+                          int64_t e_lo, int64_t e_hi, uint64_t stream_own, uint64_t stream_a, uint64_t stream_b,
                           int32_t* __restrict__ crd) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = e_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e_hi; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = row_of_entry(pos, m, e);
     int64_t k = e - pos[r], d = pos[r + 1] - pos[r];
     int64_t c;
@@ -103,7 +103,7 @@ __global__ void k_columns(int kind, int mode, int64_t m, int64_t n, uint64_t see
     else if (mode == 2 && (hash4(seed, S_REUSE_C, r, k) % 10ull) < 3ull)
       c = column_of(kind, m, n, seed, (hash4(seed, S_PICK_C, r, k) & 1ull) ? stream_b : stream_a, r, k, d);
     else c = column_of(kind, m, n, seed, stream_own, r, k, d);
-    crd[e] = (int32_t)c;
+    crd[e - e_lo] = (int32_t)c;
   }
 }
 
@@ -125,9 +125,9 @@ __device__ __forceinline__ double value_of(uint64_t seed, uint64_t stream, uint6
   return (h >> 63) ? -mag : mag;
 }
 
-__global__ void k_values(uint64_t seed, uint64_t stream, int64_t n, int mode, int kmax, int f64, void* out) {
+__global__ void k_values(uint64_t seed, uint64_t stream, int64_t i0, int64_t n, int mode, int kmax, int f64, void* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double v = value_of(seed, stream, (uint64_t)i, mode, kmax);
+    double v = value_of(seed, stream, (uint64_t)(i0 + i), mode, kmax);
     if (f64) ((double*)out)[i] = v; else ((float*)out)[i] = (float)v;
   }
 }
@@ -156,8 +156,16 @@ int wl_degrees(int64_t m, int64_t cdiv, int64_t cap, int64_t min_deg, uint64_t s
 }
 int wl_columns(int kind, int mode, int64_t m, int64_t n, uint64_t seed, const int64_t* pos, int64_t nnz,
                uint64_t stream_own, uint64_t stream_a, uint64_t stream_b, int32_t* crd, void* stream) {
-  k_columns<<<grid_for(nnz), 256, 0, (cudaStream_t)stream>>>(kind, mode, m, n, seed, pos, nnz, stream_own, stream_a,
+  k_columns<<<grid_for(nnz), 256, 0, (cudaStream_t)stream>>>(kind, mode, m, n, seed, pos, 0, nnz, stream_own, stream_a,
                                                              stream_b, crd);
+  return (int)cudaGetLastError();
+}
+// entries [e_lo, e_hi) only (a device shard's slice; pos is the full row-pointer array)
+int wl_columns_range(int kind, int mode, int64_t m, int64_t n, uint64_t seed, const int64_t* pos, int64_t e_lo,
+                     int64_t e_hi, uint64_t stream_own, uint64_t stream_a, uint64_t stream_b, int32_t* crd,
+                     void* stream) {
+  k_columns<<<grid_for(e_hi - e_lo), 256, 0, (cudaStream_t)stream>>>(kind, mode, m, n, seed, pos, e_lo, e_hi, stream_own,
+                                                                     stream_a, stream_b, crd);
   return (int)cudaGetLastError();
 }
 int wl_columns_rows(int kind, int64_t m, int64_t n, uint64_t seed, const int64_t* pos, const int32_t* outer,
@@ -166,7 +174,12 @@ int wl_columns_rows(int kind, int64_t m, int64_t n, uint64_t seed, const int64_t
   return (int)cudaGetLastError();
 }
 int wl_values(uint64_t seed, uint64_t vstream, int64_t n, int mode, int kmax, int f64, void* out, void* stream) {
-  k_values<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(seed, vstream, n, mode, kmax, f64, out);
+  k_values<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(seed, vstream, 0, n, mode, kmax, f64, out);
+  return (int)cudaGetLastError();
+}
+int wl_values_range(uint64_t seed, uint64_t vstream, int64_t i0, int64_t n, int mode, int kmax, int f64, void* out,
+                    void* stream) {
+  k_values<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(seed, vstream, i0, n, mode, kmax, f64, out);
   return (int)cudaGetLastError();
 }
 int wl_outer(int64_t m, int64_t nouter, uint64_t seed, int32_t* out, void* stream) {
