@@ -28,6 +28,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "GNNZ/s (3-way CSR SpAdd A+B+C on C2: partition + assembly + compute), % of HBM roofline"
+METRIC_C5 = "GNNZ/s (CSR SpMV y = A x on C5: partition + SpMV + carry fix-up), % of HBM roofline"
 NOMINAL_HBM_GBS = 8000.0   # north_star's "about 8 TB/s" (the roofline is also reported against it)
 
 
@@ -161,51 +162,6 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
     M = ops[0].nrows
     nnz = [A.nnz for A in ops]
     qstar = sum(nnz)
-    if world > 1:  # device-level cut: this rank runs partitions [rank*P_l, (rank+1)*P_l) of P_total
-        from paper_2604_17198_b200 import dist
-        P_l = N.auto_partitions(ops, "spadd") // world + 1
-        P = P_l * world
-        lo, hi = dist.rank_range(P, world, rank)
-        lparts = N.Parts(hi - lo, k, ops[0].pos.device)
-        l_off = torch.empty(lparts.P + 1, dtype=torch.int64, device="cuda")
-        l_ws = torch.empty(N.lib.nacho_spadd_k_staged_workspace_size(N._matrices(ops), k, lparts.P), dtype=torch.uint8,
-                           device="cuda")
-        l_pos = torch.empty(M + 1, dtype=torch.int64, device="cuda")
-        l_crd = torch.empty(qstar, dtype=torch.int32, device="cuda")
-        l_val = torch.empty(qstar, dtype=ops[0].val.dtype, device="cuda")
-
-        def step_dist(timed=False):
-            # the rank's share: its own P_l + 1 boundaries (Alg. 1 on the device cut) and the staged
-            # single-read SpAdd over them; Z stays sharded (the exchange is timed separately below)
-            m = [ev(torch)] if timed else None
-            N.partition_slice(ops, P, lo, hi, out=lparts)
-            if timed:
-                m.append(ev(torch))
-            N.spadd_k_staged(ops, lparts, l_pos, l_crd, l_val, part_off=l_off, ws=l_ws)
-            if timed:
-                m.append(ev(torch))
-            return m
-        times, sec = timer.run(step_dist, args.steps, args.warmup, ["partition_slice", "spadd_staged"], soak_s=1.0)
-        # the exchange step: all-gather of the union sizes and the Z segments, rebasing
-        import torch.distributed as tdist
-        nnz_l = int(l_off[-1].item())
-        own_lo, own_hi = int(lparts.row[0].item()), int(lparts.row[-1].item())
-        ex_ms = []
-        for _ in range(3):
-            tdist.barrier()
-            torch.cuda.synchronize()
-            e0 = ev(torch)
-            zz = dist.spadd_assemble(M, l_pos, l_crd, l_val, nnz_l, own_lo, own_hi)
-            e1 = ev(torch)
-            torch.cuda.synchronize()
-            ex_ms.append(e0.elapsed_time(e1))
-        nnz_z = int(zz[0][-1].item())
-        vs = ops[0].val.element_size()
-        algo = spadd_algo_bytes(ops, nnz_z) / world
-        return dict(work=qstar, times=times, sec=sec, launches=4, algo_step=algo, nnz_z=nnz_z, P=P,
-                    kernel_bytes={"spadd_staged": algo, "partition_slice": (lparts.P + 1) * (8 * k + 28)},
-                    two_pass={}, dtype="f32" if vs == 4 else "f64", wl=wl, parts=lparts,
-                    exchange_ms=statistics.median(ex_ms), best="spadd_staged")
     P = N.auto_partitions(ops, "spadd")
     parts = N.Parts(P, k, ops[0].pos.device)
     local = parts
@@ -310,6 +266,195 @@ def bench_spadd(N, W, torch, args, timer, world, rank):
                          "sections_ms": {s: statistics.mean(v) for s, v in sec2.items()}},
                dtype="f32" if vs == 4 else "f64", wl=wl, parts=parts, launch=launch_mode)
     return res
+
+
+def count_launches(N, torch, step):
+    """Kernels (and memsets) the library issues in one step (its own launch counter)."""
+    torch.cuda.synchronize()
+    N.launch_count(reset=True)
+    step()
+    torch.cuda.synchronize()
+    return N.launch_count(reset=True)
+
+
+class Exchange:
+    """The exchange step of the multi-GPU path: libnacho's NCCL calls (nacho_dist_*), or -- for
+    one-GPU smoke runs of the N > 1 code path (NACHO_DIST_BACKEND=gloo, several ranks on one device,
+    which NCCL refuses) -- the same data movement through torch.distributed."""
+
+    def __init__(self, N, torch, backend):
+        self.N, self.torch, self.backend = N, torch, backend
+        import torch.distributed as td
+        self.td = td
+        self.world, self.rank = td.get_world_size(), td.get_rank()
+        self.comm = N.Dist.from_process_group() if backend == "nccl" else None
+
+    def broadcast(self, t, root=0):
+        if self.comm:
+            self.comm.broadcast(t, root)
+        else:
+            c = t.cpu()
+            self.td.broadcast(c, src=root)
+            t.copy_(c)
+
+    def spmv(self, A_loc, parts, x, y_loc, plans, y_full=None):
+        N, torch = self.N, self.torch
+        D = self.N_dist()
+        if self.comm:
+            return self.comm.spmv(A_loc, parts, x, y_loc, D.cut_rows(plans, plans[-1].row_lo + plans[-1].own),
+                                  y_full=y_full)
+        p = plans[self.rank]
+        if p.nloc > 0:
+            N.spmv(A_loc, x, parts, y=y_loc[:p.nloc])
+        r, b = D.carry_of(p, y_loc)
+        mine = torch.cat([r, b]).cpu()
+        allc = [torch.empty_like(mine) for _ in range(self.world)]
+        self.td.all_gather(allc, mine)
+        if p.nloc > 0:
+            N.dist_seam(torch.stack(allc).cuda().contiguous(), self.world, self.rank, p.row_lo, p.own > 0, y_loc)
+        if y_full is not None:
+            segs = [None] * self.world
+            self.td.all_gather_object(segs, (p.row_lo, y_loc[:p.own].cpu()))
+            for lo, seg in segs:
+                y_full[lo:lo + len(seg)] = seg.to(y_full.device)
+        return y_loc
+
+    def spadd_gather(self, zp, zc, zv, nnz_dev, cut_rows, z_pos, z_crd, z_val):
+        if self.comm:
+            return self.comm.spadd_gather(zp, zc, zv, nnz_dev, cut_rows, z_pos, z_crd, z_val)
+        torch = self.torch
+        d = self.rank
+        own = cut_rows[d + 1] - cut_rows[d]
+        n = int(nnz_dev.item())
+        pieces = [None] * self.world
+        self.td.all_gather_object(pieces, (n, zp[1:own + 1].cpu(), zc[:n].cpu(), zv[:n].cpu()))
+        base = 0
+        z_pos[0] = 0
+        for r, (nr, rows, c, v) in enumerate(pieces):
+            z_pos[cut_rows[r] + 1:cut_rows[r] + 1 + len(rows)] = rows.to(z_pos.device) + base
+            z_crd[base:base + nr] = c.to(z_crd.device)
+            z_val[base:base + nr] = v.to(z_val.device)
+            base += nr
+        return base
+
+    def N_dist(self):
+        from paper_2604_17198_b200 import dist as D
+        return D
+
+    def close(self):
+        if self.comm:
+            self.comm.close()
+
+
+def bench_spadd_dist(N, W, torch, args, timer, ex):
+    """C2 on D devices: Alg. 1 with P = D gives the device cuts; each rank holds its
+    operand shards (rows of its coordinate range, nacho_shard_rows) and runs its own partitions of them
+    (partition + single-read SpAdd) -- timed, kernel-only; the exchange (nacho_dist_spadd_gather: union
+    sizes -> offsets, Z segments gathered) is timed separately."""
+    from paper_2604_17198_b200 import dist as D
+    world, rank = ex.world, ex.rank
+    wl = W.build("c2", args.scale, device="cuda")
+    ops = wl.ops
+    k = len(ops)
+    M = ops[0].nrows
+    qstar = sum(A.nnz for A in ops)
+    dparts = N.partition(ops, world)
+    sh, row_lo, own = D.spadd_shard_ops(ops, dparts, rank)
+    cut_rows = [int(r) for r in dparts.row.cpu().tolist()]
+    cut_rows[-1] = M
+    P_l = N.auto_partitions(sh, "spadd")
+    parts = N.Parts(P_l, k, "cuda")
+    off = torch.empty(P_l + 1, dtype=torch.int64, device="cuda")
+    cap = sum(A.nnz for A in sh)
+    z_pos = torch.empty(sh[0].nrows + 1, dtype=torch.int64, device="cuda")
+    z_crd = torch.empty(max(cap, 1), dtype=torch.int32, device="cuda")
+    z_val = torch.empty(max(cap, 1), dtype=ops[0].val.dtype, device="cuda")
+    ws = torch.empty(N.lib.nacho_spadd_k_workspace_size(N._matrices(sh), k, P_l), dtype=torch.uint8, device="cuda")
+
+    def step(timed=False):
+        m = [ev(torch)] if timed else None
+        N.partition(sh, P_l, out=parts)
+        if timed:
+            m.append(ev(torch))
+        N.spadd_k_fused(sh, parts, z_pos, z_crd, z_val, part_off=off, ws=ws)
+        if timed:
+            m.append(ev(torch))
+        return m
+    times, sec = timer.run(step, args.steps, args.warmup, ["partition", "spadd_fused"], soak_s=1.0)
+    # the exchange step, timed separately (max over ranks by the caller's all-reduce of the median)
+    zf_pos = torch.empty(M + 1, dtype=torch.int64, device="cuda")
+    zf_crd = torch.empty(qstar, dtype=torch.int32, device="cuda")
+    zf_val = torch.empty(qstar, dtype=ops[0].val.dtype, device="cuda")
+    ex_ms = []
+    nnz_z = 0
+    for _ in range(3):
+        ex.td.barrier()
+        torch.cuda.synchronize()
+        e0 = ev(torch)
+        nnz_z = ex.spadd_gather(z_pos, z_crd, z_val, off[-1:], cut_rows, zf_pos, zf_crd, zf_val)
+        e1 = ev(torch)
+        torch.cuda.synchronize()
+        ex_ms.append(e0.elapsed_time(e1))
+    algo = spadd_algo_bytes(ops, nnz_z) / world
+    return dict(work=qstar, times=times, sec=sec, launches=count_launches(N, torch, step), algo_step=algo,
+                nnz_z=nnz_z, P=P_l * world, kernel_bytes={"spadd_fused": algo, "partition": (P_l + 1) * (8 * k + 28)},
+                two_pass={}, dtype="f32", wl=wl, exchange_ms=statistics.median(ex_ms), best="spadd_fused",
+                shard={"rows": [row_lo, row_lo + own], "entries": cap})
+
+
+def bench_spmv_dist(N, W, torch, args, timer, ex):
+    """C5 on D devices: every rank builds only its shard (device cuts from the row pointers,
+    nacho_device_cuts; its entries generated in place), x broadcast at setup (timed separately); timed:
+    the rank's partition + nacho_dist_spmv (local SpMV + seam-carry all-gather + fix-up); the gather of
+    the owned y segments is timed separately (exchange_ms)."""
+    from paper_2604_17198_b200 import dist as D
+    world, rank = ex.world, ex.rank
+    t0 = time.perf_counter()
+    A_loc, plans, cuts = D.spmv_setup("c5", args.scale, world, rank)
+    M = plans[-1].row_lo + plans[-1].own
+    nnz_total = int(cuts[-1][1])
+    x = W.dense_x("c5", args.scale) if rank == 0 else torch.empty(M, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    ex.td.barrier()
+    e0 = ev(torch)
+    ex.broadcast(x, 0)
+    e1 = ev(torch)
+    torch.cuda.synchronize()
+    bcast_ms = e0.elapsed_time(e1)
+    setup_s = time.perf_counter() - t0
+    p = plans[rank]
+    P_l = N.auto_partitions([A_loc], "spmv")
+    parts = N.Parts(P_l, 1, "cuda")
+    y_loc = torch.empty(max(p.nloc, 1), dtype=torch.float32, device="cuda")
+
+    def step(timed=False):
+        m = [ev(torch)] if timed else None
+        N.partition([A_loc], P_l, out=parts)
+        if timed:
+            m.append(ev(torch))
+        ex.spmv(A_loc, parts, x, y_loc, plans)
+        if timed:
+            m.append(ev(torch))
+        return m
+    times, sec = timer.run(step, args.steps, args.warmup, ["partition", "spmv+seam"], soak_s=1.0)
+    y_full = torch.empty(M, dtype=torch.float32, device="cuda")
+    gx = []
+    for _ in range(3):
+        ex.td.barrier()
+        torch.cuda.synchronize()
+        e0 = ev(torch)
+        ex.spmv(A_loc, parts, x, y_loc, plans, y_full=y_full)
+        e1 = ev(torch)
+        torch.cuda.synchronize()
+        gx.append(e0.elapsed_time(e1))
+    nnz = A_loc.nnz
+    algo = nnz * 8 + (p.nloc + 1) * 8 + p.nloc * 4 + M * 4
+    return dict(work=nnz_total, times=times, sec=sec, launches=count_launches(N, torch, step), algo_step=algo,
+                nnz_z=0, P=P_l * world,
+                kernel_bytes={"spmv+seam": algo, "partition": (P_l + 1) * 36}, two_pass={}, dtype="f32", wl=None,
+                exchange_ms=statistics.median(gx) - statistics.median(sec["spmv+seam"]),
+                shard={"rows": [p.row_lo, p.row_lo + p.own], "entries": nnz}, setup={"x_broadcast_ms": bcast_ms,
+                                                                                     "setup_s": setup_s})
 
 
 def e2e_spadd(N, torch, wl, args, staged):
@@ -625,7 +770,17 @@ def main():
     timer = Timer(torch, max(2 * l2, 256 << 20))
 
     clocks = Clocks(local)
-    r = bench_spadd(N, W, torch, args, timer, world, rank)
+    ex = Exchange(N, torch, os.environ.get("NACHO_DIST_BACKEND", "nccl")) if world > 1 else None
+    if args.workload == "c2":
+        r = bench_spadd_dist(N, W, torch, args, timer, ex) if world > 1 else bench_spadd(N, W, torch, args, timer, 1, 0)
+        metric, wname = METRIC, "c2_spadd3_1Mx1M_3x1e7nnz"
+    else:
+        if world > 1:
+            r = bench_spmv_dist(N, W, torch, args, timer, ex)
+        else:
+            r = bench_spmv(N, W, torch, "c5", args.scale, args.steps, args.warmup, timer)
+            r["launches"] = 3
+        metric, wname = METRIC_C5, "c5_spmv_csr_f32_200Mx200M_4e9nnz"
     clk = clocks.stop()
 
     times = r["times"]
@@ -633,44 +788,54 @@ def main():
     ms = ms_local
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms_local], device="cuda")
+        t = torch.tensor([ms_local, r.get("exchange_ms") or 0.0], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(t[0].item())
+        r["exchange_ms"] = float(t[1].item())
     summ, dom, dms, achieved = summarize(r, peak)
-    tt = traffic_table().get(f"c2:{dom}") if world == 1 else None   # table holds single-GPU launches
+    tt = traffic_table().get(f"{args.workload}:{dom}") if world == 1 else None   # table holds single-GPU launches
+    work = r["work"]
     line = {
-        "metric": METRIC,
-        "value": sum(A.nnz for A in r["wl"].ops) / (ms * 1e-3) / 1e9,
+        "metric": metric,
+        "value": work / (ms * 1e-3) / 1e9,
         "unit": "GNNZ/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
         "dtype": r["dtype"], "data": "synthetic (seeded power-law CSR, workloads/ recipe)",
-        "config": {"workload": "c2_spadd3_1Mx1M_3x1e7nnz", "k": 3, "nnz_per_operand": r["wl"].ops[0].nnz,
-                   "nnz_Z": r["nnz_z"], "P": r["P"], "scale": args.scale,
+        "config": {"workload": wname, "scale": args.scale, "P": r["P"],
                    "l2": "flushed between timed steps (untimed memset of 2x L2)", "parallelism": f"dp{world}",
                    "launch": r.get("launch", "eager"),
-                   **({"z_output": "sharded across ranks (device cut of Alg. 1); the all-gather of Z is timed "
-                                   "separately as exchange_ms"} if world > 1 else {})},
+                   **({"k": 3, "nnz_per_operand": r["wl"].ops[0].nnz, "nnz_Z": r["nnz_z"]}
+                      if args.workload == "c2" and r.get("wl") is not None else {}),
+                   **({"sharding": "device cuts = Alg. 1 with P = D; each rank holds and computes only its shard; "
+                                   "value = kernel-only time (max over ranks); the output exchange is timed "
+                                   "separately as exchange_ms", "exchange": ex.backend,
+                       "shard_rank0": r.get("shard"), "setup": r.get("setup")} if world > 1 else {})},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "frac_nominal_8tbs": achieved / NOMINAL_HBM_GBS, "traffic": tt,
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": r["kernel_bytes"][dom]},
         "step_roofline_frac": summ["step_hbm_frac"],
         "sections_ms": summ["sections_ms"],
-        "two_pass": r["two_pass"],
+        "two_pass": r.get("two_pass"),
         "single_read_variants_ms": r.get("variants_ms"),
         "exchange_ms": r.get("exchange_ms"),
+        "end_to_end_ms": (ms + r["exchange_ms"]) if world > 1 else None,
         "gpu_launches": r["launches"] * args.steps,
         "clocks": clk,
     }
-    if rank == 0 and world == 1 and not args.no_e2e:
+    if rank == 0 and world == 1 and not args.no_e2e and args.workload == "c2":
         line["e2e"] = e2e_spadd(N, torch, r["wl"], args, r.get("best") == "spadd_staged")
     if rank == 0 and world == 1 and not args.no_cpu:
-        host = [A.numpy() for A in r["wl"].ops]
-        line["cpu_baseline"] = cpu_baseline(host, r["P"])
-    wl_keep = r.pop("wl")
+        if args.workload == "c2":
+            line["cpu_baseline"] = cpu_baseline([A.numpy() for A in r["wl"].ops], r["P"])
+        else:
+            line["cpu_baseline"] = cpu_baseline_spmv(r["wl"].ops[0], r["wl"].x, r["P"])
+    if world > 1 and ex is not None:
+        ex.close()
+    wl_keep = r.pop("wl", None)
     del wl_keep, r
     torch.cuda.empty_cache()
-    if not args.quick and world == 1:
+    if not args.quick and world == 1 and args.workload == "c2":
         kern = {}
         for name, fn in [("c5_spmv_csr_f32", lambda: bench_spmv(N, W, torch, "c5", args.scale, 10, 3, timer)),
                          ("c3_spmv_dcsr_f32", lambda: bench_spmv(N, W, torch, "c3", args.scale, 10, 3, timer)),
