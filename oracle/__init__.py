@@ -58,6 +58,10 @@ def lib():
         L.oracle_spadd_k.argtypes = [ctypes.c_int32, vp, vp, vp, vp, ctypes.c_int64]
         L.oracle_spadd_k.restype = ctypes.c_int64
         L.oracle_spadd_counts.argtypes = [ctypes.c_int32, vp, vp, vp]
+        L.oracle_hadamard_k.argtypes = [ctypes.c_int32, vp, vp, vp, vp, ctypes.c_int64]
+        L.oracle_hadamard_k.restype = ctypes.c_int64
+        L.oracle_hadamard_counts.argtypes = [ctypes.c_int32, vp, vp, vp]
+        L.oracle_inner_k.argtypes = [ctypes.c_int32, vp, vp]
     return _lib
 
 
@@ -184,3 +188,35 @@ def spadd_counts(ops, parts: Parts) -> np.ndarray:
     if lib().oracle_spadd_counts(len(ops), arr, ctypes.byref(s), _p(cnt)) != 0:
         raise ValueError("oracle_spadd_counts failed")
     return cnt
+
+
+def hadamard_k(ops):
+    """(z_pos, z_crd, z_val) of the k-way structural intersection (Listing 1 per row), product values."""
+    arr, keep = _matrices(ops)
+    cap = int(min(int(A.crd.shape[0]) for A in ops))
+    M = ops[0].nrows
+    z_pos = np.zeros(M + 1, np.int64)
+    z_crd = np.zeros(max(cap, 1), np.int32)
+    z_val = np.zeros(max(cap, 1), dtype=ops[0].val.dtype)
+    n = lib().oracle_hadamard_k(len(ops), arr, _p(z_pos), _p(z_crd), _p(z_val), cap)
+    if n < 0:
+        raise ValueError("oracle_hadamard_k failed")
+    return z_pos, z_crd[:n].copy(), z_val[:n].copy()
+
+
+def hadamard_counts(ops, parts: Parts) -> np.ndarray:
+    arr, keep = _matrices(ops)
+    cnt = np.zeros(parts.P, np.int64)
+    s = parts.c()
+    if lib().oracle_hadamard_counts(len(ops), arr, ctypes.byref(s), _p(cnt)) != 0:
+        raise ValueError("oracle_hadamard_counts failed")
+    return cnt
+
+
+def inner_k(ops) -> float:
+    arr, keep = _matrices(ops)
+    out = ctypes.c_double(0.0)
+    if lib().oracle_inner_k(len(ops), arr, ctypes.byref(out)) != 0:
+        raise ValueError("oracle_inner_k failed")
+    return float(out.value)
+

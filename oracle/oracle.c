@@ -341,3 +341,117 @@ int oracle_spadd_counts(int32_t k, const or_matrix *ops, const or_parts *parts, 
     free(q);
     return 0;
 }
+
+/* ------------------------------------------------------ k-way intersection */
+/*
+ * Z = A_0 (.) ... (.) A_{k-1} (element-wise product): the k-finger merge of Listing 1 (P:333-344,
+ * "z_i = a_i * b_i * c_i via a three-finger merge") applied to every CSR row, which is the loop body of
+ * the partitioned CSR Hadamard product of Listing 8 run with one partition.  A
+ * coordinate is emitted when every operand's head equals the minimum head (Listing 1 line "if i ==
+ * i_a && i == i_b && i == i_c"); every finger whose head equals the minimum advances.  Z.val is the
+ * product in operand order, left to right, in the value type's own arithmetic (Listing 1 evaluates
+ * a.v * b.v * c.v as (a.v * b.v) * c.v).  Structure is the structural intersection (stored entries,
+ * whatever their values).
+ */
+int64_t oracle_hadamard_k(int32_t k, const or_matrix *ops, int64_t *z_pos, int32_t *z_crd, void *z_val,
+                          int64_t capacity) {
+    for (int32_t o = 0; o < k; o++) if (ops[o].format != OR_CSR) return -1;
+    const int64_t M = ops[0].nrows;
+    const int f64 = ops[0].dtype == OR_F64;
+    int64_t *q = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    int64_t nz = 0;
+    z_pos[0] = 0;
+    for (int64_t i = 0; i < M; i++) {
+        for (int32_t o = 0; o < k; o++) q[o] = ops[o].pos[i];
+        for (;;) {
+            /* while p_a < nnz(a) && p_b < nnz(b) && ... (all fingers inside their row segments) */
+            int inside = 1;
+            for (int32_t o = 0; o < k; o++) if (q[o] >= ops[o].pos[i + 1]) inside = 0;
+            if (!inside) break;
+            int64_t j = ops[0].crd[q[0]];
+            for (int32_t o = 1; o < k; o++) if (ops[o].crd[q[o]] < j) j = ops[o].crd[q[o]];
+            int all = 1;
+            for (int32_t o = 0; o < k; o++) if (ops[o].crd[q[o]] != j) all = 0;
+            if (all) {
+                if (nz >= capacity) { free(q); return -1; }
+                if (f64) {
+                    double v = ((const double *)ops[0].val)[q[0]];
+                    for (int32_t o = 1; o < k; o++) v = v * ((const double *)ops[o].val)[q[o]];
+                    ((double *)z_val)[nz] = v;
+                } else {
+                    float v = ((const float *)ops[0].val)[q[0]];
+                    for (int32_t o = 1; o < k; o++) v = v * ((const float *)ops[o].val)[q[o]];
+                    ((float *)z_val)[nz] = v;
+                }
+                z_crd[nz++] = (int32_t)j;
+            }
+            for (int32_t o = 0; o < k; o++) if (ops[o].crd[q[o]] == j) q[o]++;
+        }
+        z_pos[i + 1] = nz;
+    }
+    free(q);
+    return nz;
+}
+
+/* Per-partition assembly counts of the intersection (P:2051-2056 with the intersection predicate):
+ * cnt[p] = #coordinates c stored by every operand with b_p <=lex c <lex b_{p+1}. */
+int oracle_hadamard_counts(int32_t k, const or_matrix *ops, const or_parts *parts, int64_t *cnt) {
+    for (int32_t o = 0; o < k; o++) if (ops[o].format != OR_CSR) return 1;
+    const int32_t P = parts->P;
+    const int64_t M = ops[0].nrows;
+    int64_t *q = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    for (int32_t p = 0; p < P; p++) cnt[p] = 0;
+    int32_t p = 0;
+    for (int64_t i = 0; i < M; i++) {
+        for (int32_t o = 0; o < k; o++) q[o] = ops[o].pos[i];
+        for (;;) {
+            int inside = 1;
+            for (int32_t o = 0; o < k; o++) if (q[o] >= ops[o].pos[i + 1]) inside = 0;
+            if (!inside) break;
+            int64_t j = ops[0].crd[q[0]];
+            for (int32_t o = 1; o < k; o++) if (ops[o].crd[q[o]] < j) j = ops[o].crd[q[o]];
+            int all = 1;
+            for (int32_t o = 0; o < k; o++) if (ops[o].crd[q[o]] != j) all = 0;
+            if (all) {
+                while (p + 1 < P && (i > parts->row[p + 1] || (i == parts->row[p + 1] && j >= parts->col[p + 1]))) p++;
+                cnt[p]++;
+            }
+            for (int32_t o = 0; o < k; o++) if (ops[o].crd[q[o]] == j) q[o]++;
+        }
+    }
+    free(q);
+    return 0;
+}
+
+/* The intersect-reduce inner product s = sum_(i,j) prod_o A_o(i,j) (the fused (.) + reduction of
+ * the paper's inner-product evaluation, on CSR operands): the same k-finger merge, every
+ * product and the sum accumulated wide (long double), rounded once (reading R13: summation order
+ * free within tolerance). */
+int oracle_inner_k(int32_t k, const or_matrix *ops, double *out) {
+    for (int32_t o = 0; o < k; o++) if (ops[o].format != OR_CSR) return 1;
+    const int64_t M = ops[0].nrows;
+    int64_t *q = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    long double s = 0.0L;
+    for (int64_t i = 0; i < M; i++) {
+        for (int32_t o = 0; o < k; o++) q[o] = ops[o].pos[i];
+        for (;;) {
+            int inside = 1;
+            for (int32_t o = 0; o < k; o++) if (q[o] >= ops[o].pos[i + 1]) inside = 0;
+            if (!inside) break;
+            int64_t j = ops[0].crd[q[0]];
+            for (int32_t o = 1; o < k; o++) if (ops[o].crd[q[o]] < j) j = ops[o].crd[q[o]];
+            int all = 1;
+            for (int32_t o = 0; o < k; o++) if (ops[o].crd[q[o]] != j) all = 0;
+            if (all) {
+                long double v = 1.0L;
+                for (int32_t o = 0; o < k; o++) v *= vget_ld(&ops[o], q[o]);
+                s += v;
+            }
+            for (int32_t o = 0; o < k; o++) if (ops[o].crd[q[o]] == j) q[o]++;
+        }
+    }
+    free(q);
+    *out = (double)s;
+    return 0;
+}
+

@@ -71,6 +71,15 @@ int64_t oracle_spadd_k(int32_t k, const or_matrix *ops, int64_t *z_pos, int32_t 
 /* Per-partition union counts for given boundaries: cnt[p] = #union coordinates c with b_p <=lex c <lex b_{p+1}. */
 int     oracle_spadd_counts(int32_t k, const or_matrix *ops, const or_parts *parts, int64_t *cnt);
 
+/* Z = ops[0] (.) ... (.) ops[k-1] (k-way structural intersection, CSR; Listing 1's k-finger merge per
+ * row).  Values: product in operand order, left to right, in the value type.  Returns nnz_Z, or -1. */
+int64_t oracle_hadamard_k(int32_t k, const or_matrix *ops, int64_t *z_pos, int32_t *z_crd, void *z_val,
+                          int64_t capacity);
+/* Per-partition intersection counts for given boundaries. */
+int     oracle_hadamard_counts(int32_t k, const or_matrix *ops, const or_parts *parts, int64_t *cnt);
+/* s = sum over the intersection of the products (wide accumulation, rounded once to double). */
+int     oracle_inner_k(int32_t k, const or_matrix *ops, double *out);
+
 #ifdef __cplusplus
 }
 #endif
