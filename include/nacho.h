@@ -181,6 +181,31 @@ nacho_status nacho_spmm(const nacho_matrix* A, const nacho_parts* parts, const v
                         void* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------------------------
+ * k-way intersection kernels on the same partitioner (a1-a5): Alg. 1 over the
+ * operands' entries is exact for a coiteration that walks every operand's entries, and
+ * equal coordinates never straddle a cut, so every output coordinate is produced
+ * inside one partition.  The merge predicate is Listing 1's (emit when every head equals
+ * the minimum) instead of the union's.  CSR operands, k <= 4, partitions of at most
+ * nacho_auto_partitions(ops, k, 1)'s size.
+ *
+ * nacho_hadamard_k -- Z = ops[0] (.) ... (.) ops[k-1], the partitioned CSR Hadamard product of
+ * Listing 8 in one pass (assembly count, decoupled look-back offsets, fill): Z.pos
+ * [nrows+1]; Z.crd / Z.val with capacity >= min_o nnz_o (nnz_Z = z_pos[nrows]); values are the product
+ * in operand order, left to right, in the value type (bit-identical to Listing 1's a.v * b.v * c.v).
+ * part_off (optional, [P+1]) receives the per-partition offsets.  Workspace:
+ * nacho_spadd_k_workspace_size. */
+nacho_status nacho_hadamard_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
+                              int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes, void* stream);
+
+/* nacho_inner_k -- the intersect-reduce inner product s = sum_(i,j) prod_o ops[o](i,j) (the fused
+ * (.) + reduction of the paper's inner-product evaluation, on CSR operands): products as
+ * in nacho_hadamard_k, summed in fp64 per partition and then over partitions in a fixed order
+ * (deterministic).  result: device double[1]. */
+size_t nacho_inner_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P);
+nacho_status nacho_inner_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, double* result, void* ws,
+                           size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
  * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.
  * Synchronous on `stream` (it reads one flag back).  Returns NACHO_ERR_FORMAT on a violation. */
 nacho_status nacho_validate(const nacho_matrix* A, void* stream);

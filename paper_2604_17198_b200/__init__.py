@@ -70,6 +70,10 @@ def _load():
     L.nacho_last_error.restype = ctypes.c_char_p
     L.nacho_launch_count.argtypes = [i32]
     L.nacho_launch_count.restype = i64
+    L.nacho_hadamard_k.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_inner_k_workspace_size.argtypes = [vp, i32, i32]
+    L.nacho_inner_k_workspace_size.restype = sz
+    L.nacho_inner_k.argtypes = [vp, i32, vp, vp, vp, sz, vp]
     # multi-GPU (dist.cuh)
     L.nacho_dist_unique_id_size.restype = sz
     L.nacho_dist_unique_id.argtypes = [vp]
@@ -94,7 +98,8 @@ EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", 
            "nacho_spadd_k_workspace_size", "nacho_spadd_k_count", "nacho_spadd_k_fill", "nacho_spadd_k",
            "nacho_spadd_k_staged_workspace_size", "nacho_spadd_k_staged",
            "nacho_spmm_workspace_size", "nacho_spmm", "nacho_validate", "nacho_last_error",
-           "nacho_launch_count", "nacho_dist_unique_id_size", "nacho_dist_unique_id", "nacho_dist_init",
+           "nacho_launch_count", "nacho_hadamard_k", "nacho_inner_k_workspace_size", "nacho_inner_k",
+           "nacho_dist_unique_id_size", "nacho_dist_unique_id", "nacho_dist_init",
            "nacho_dist_destroy", "nacho_dist_broadcast", "nacho_device_cuts", "nacho_shard_rows", "nacho_dist_seam",
            "nacho_dist_spmv_workspace_size", "nacho_dist_spmv", "nacho_dist_spadd_workspace_size",
            "nacho_dist_spadd_gather"]
@@ -323,6 +328,41 @@ def validate(A, stream=None):
 
 def launch_count(reset: bool = False) -> int:
     return lib.nacho_launch_count(int(reset))
+
+
+# ------------------------------------------------------------------ k-way intersection
+def hadamard_k(ops, parts: Parts, z_pos=None, z_crd=None, z_val=None, part_off=None, ws=None, stream=None):
+    """nacho_hadamard_k: Z = ops[0] (.) ... (.) ops[k-1] in one pass.  z_crd / z_val at capacity
+    min_o nnz_o; nnz_Z = z_pos[-1]."""
+    arr = _matrices(ops)
+    dev = ops[0].pos.device
+    cap = max(1, min(int(A.crd.shape[0]) for A in ops))
+    if z_pos is None:
+        z_pos = torch.empty(ops[0].nrows + 1, dtype=torch.int64, device=dev)
+    if z_crd is None:
+        z_crd = torch.empty(cap, dtype=torch.int32, device=dev)
+    if z_val is None:
+        z_val = torch.empty(cap, dtype=ops[0].val.dtype, device=dev)
+    need = lib.nacho_spadd_k_workspace_size(arr, len(ops), parts.P)
+    if ws is None or ws.numel() < need:
+        ws, _ = _workspace(need, dev)
+    pc = parts.c()
+    _check(lib.nacho_hadamard_k(arr, len(ops), ctypes.byref(pc), _ptr(part_off), _ptr(z_pos), _ptr(z_crd), _ptr(z_val),
+                                _ptr(ws), need, _stream(stream)))
+    return z_pos, z_crd, z_val
+
+
+def inner_k(ops, parts: Parts, out=None, ws=None, stream=None) -> torch.Tensor:
+    """nacho_inner_k: sum over the intersection of the products (device double[1])."""
+    arr = _matrices(ops)
+    dev = ops[0].pos.device
+    out = out if out is not None else torch.empty(1, dtype=torch.float64, device=dev)
+    need = lib.nacho_inner_k_workspace_size(arr, len(ops), parts.P)
+    if ws is None or ws.numel() < need:
+        ws, _ = _workspace(need, dev)
+    pc = parts.c()
+    _check(lib.nacho_inner_k(arr, len(ops), ctypes.byref(pc), _ptr(out), _ptr(ws), need, _stream(stream)))
+    return out
 
 
 # ------------------------------------------------------------------ multi-GPU (include/nacho.h, dist.cuh)

@@ -477,9 +477,9 @@ nacho_status run_spadd5(const nacho_matrix* ops, int32_t k, const nacho_parts* p
 }
 
 // Pipelined single-read SpAdd (spadd7.cuh): producer / compute / emission warps over NS stages.
-template <typename T, int K>
+template <typename T, int K, int OP = kS7Union>
 nacho_status launch_spadd7_k(const S7Args<T>& a, cudaStream_t st) {
-  auto kern = spadd7_kernel<T, K>;
+  auto kern = spadd7_kernel<T, K, OP>;
   const size_t smem = sizeof(S7Smem<T, K>);
   static std::atomic<uint64_t> done{0};
   NACHO_TRY(smem_optin(kern, smem, done, "spadd7_kernel"));
@@ -493,9 +493,9 @@ nacho_status launch_spadd7_k(const S7Args<T>& a, cudaStream_t st) {
   return launched("spadd7_kernel");
 }
 
-template <typename T>
+template <typename T, int OP = kS7Union>
 nacho_status run_spadd7(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off, int64_t* z_pos,
-                        int32_t* z_crd, T* z_val, unsigned long long* state, cudaStream_t st) {
+                        int32_t* z_crd, T* z_val, unsigned long long* state, cudaStream_t st, double* partial = nullptr) {
   S7Args<T> a;
   memset(&a, 0, sizeof(a));
   a.ops = make_ops(ops, k);
@@ -522,6 +522,7 @@ nacho_status run_spadd7(const nacho_matrix* ops, int32_t k, const nacho_parts* p
   a.z_pos = z_pos;
   a.z_crd = z_crd;
   a.z_val = z_val;
+  a.partial = partial;
 #ifdef NACHO_S7_PROF
   const int nclear = parts->P + 2 + 16;
 #else
@@ -529,15 +530,25 @@ nacho_status run_spadd7(const nacho_matrix* ops, int32_t k, const nacho_parts* p
 #endif
   if (cudaMemsetAsync(state, 0, sizeof(unsigned long long) * nclear, st) != cudaSuccess)
     return fail(NACHO_ERR_CUDA, "memset look-back states");
-  switch (k) {
-    case 1: return launch_spadd7_k<T, 1>(a, st);
-    case 2: return launch_spadd7_k<T, 2>(a, st);
-    case 3: return launch_spadd7_k<T, 3>(a, st);
-    case 4: return launch_spadd7_k<T, 4>(a, st);
-    case 5: return launch_spadd7_k<T, 5>(a, st);
-    case 6: return launch_spadd7_k<T, 6>(a, st);
-    case 7: return launch_spadd7_k<T, 7>(a, st);
-    default: return launch_spadd7_k<T, 8>(a, st);
+  if constexpr (OP != kS7Union) {   // intersections: k <= 4 instantiated
+    switch (k) {
+      case 1: return launch_spadd7_k<T, 1, OP>(a, st);
+      case 2: return launch_spadd7_k<T, 2, OP>(a, st);
+      case 3: return launch_spadd7_k<T, 3, OP>(a, st);
+      case 4: return launch_spadd7_k<T, 4, OP>(a, st);
+      default: return fail(NACHO_ERR_INVALID_ARG, "intersection kernels take k <= 4 operands (k = %d)", k);
+    }
+  } else {
+    switch (k) {
+      case 1: return launch_spadd7_k<T, 1>(a, st);
+      case 2: return launch_spadd7_k<T, 2>(a, st);
+      case 3: return launch_spadd7_k<T, 3>(a, st);
+      case 4: return launch_spadd7_k<T, 4>(a, st);
+      case 5: return launch_spadd7_k<T, 5>(a, st);
+      case 6: return launch_spadd7_k<T, 6>(a, st);
+      case 7: return launch_spadd7_k<T, 7>(a, st);
+      default: return launch_spadd7_k<T, 8>(a, st);
+    }
   }
 }
 
@@ -554,6 +565,53 @@ int spadd_impl() {
 }  // namespace
 
 extern "C" {
+
+/* ------------------------------------------------------------------ k-way intersection (spadd7, OP) */
+static nacho_status check_intersection(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, cudaStream_t st) {
+  NACHO_TRY(check_ops(ops, k));
+  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "intersection kernels take CSR operands");
+  if (k > 4) return fail(NACHO_ERR_INVALID_ARG, "intersection kernels take k <= 4 operands (k = %d)", k);
+  NACHO_TRY(check_parts(parts, k));
+  if (!spadd5_applies(ops, k, parts_arg(parts), st))
+    return fail(NACHO_ERR_INVALID_ARG, "partitions larger than %d entries (or > 2^24 columns): use P >= "
+                "nacho_auto_partitions(ops, k, 1)", s5_max_entries(k));
+  return NACHO_SUCCESS;
+}
+
+nacho_status nacho_hadamard_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
+                              int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  NACHO_TRY(check_intersection(ops, k, parts, st));
+  if (!z_pos) return fail(NACHO_ERR_INVALID_ARG, "null z_pos");
+  if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
+  const size_t need = nacho_spadd_k_workspace_size(ops, k, parts->P);
+  if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  auto* flags = static_cast<unsigned long long*>(ws);
+  if (ops[0].dtype == NACHO_F64)
+    return run_spadd7<double, kS7Inter>(ops, k, parts, part_off, z_pos, z_crd, static_cast<double*>(z_val), flags, st);
+  return run_spadd7<float, kS7Inter>(ops, k, parts, part_off, z_pos, z_crd, static_cast<float*>(z_val), flags, st);
+}
+
+size_t nacho_inner_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {
+  return nacho_spadd_k_workspace_size(ops, k, P) + align_up((size_t)(P > 0 ? P : 1) * 8);
+}
+
+nacho_status nacho_inner_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, double* result, void* ws,
+                           size_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  NACHO_TRY(check_intersection(ops, k, parts, st));
+  if (!result) return fail(NACHO_ERR_INVALID_ARG, "null result");
+  const size_t need = nacho_inner_k_workspace_size(ops, k, parts->P);
+  if (ws_bytes < need || !ws) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  auto* flags = static_cast<unsigned long long*>(ws);
+  double* partial = reinterpret_cast<double*>(static_cast<char*>(ws) + nacho_spadd_k_workspace_size(ops, k, parts->P));
+  nacho_status r = ops[0].dtype == NACHO_F64
+                       ? run_spadd7<double, kS7InterSum>(ops, k, parts, nullptr, nullptr, nullptr, nullptr, flags, st, partial)
+                       : run_spadd7<float, kS7InterSum>(ops, k, parts, nullptr, nullptr, nullptr, nullptr, flags, st, partial);
+  NACHO_TRY(r);
+  s7_sum_partials_kernel<<<1, 1024, 0, st>>>(partial, parts->P, result);
+  return launched("s7_sum_partials_kernel");
+}
 
 /* ------------------------------------------------------------------ multi-GPU (dist.cuh) */
 #define NACHO_NCCL(call)                                                                              \

@@ -37,6 +37,11 @@ constexpr int kS7Slots = kS5Slots;           // shared-memory slots per stage (e
 constexpr int kS7PosPool = 384;              // row-pointer pool per stage (int64 words)
 constexpr int kS7LMax = kS7PosPool - 2;      // rows per (sub-)tile, one distinct pos array
 
+// The coiteration the kernel runs over a partition (P:2051-2061 assembly, P:2145-2150 compute):
+constexpr int kS7Union = 0;      // k-way SpAdd: union of coordinates, values summed (Listing 2)
+constexpr int kS7Inter = 1;      // k-way Hadamard: intersection, values multiplied (Listings 1 and 8)
+constexpr int kS7InterSum = 2;   // intersect-reduce inner product: sum of the intersection's products
+
 template <typename V, int K>
 struct S7Cfg {
 #ifdef NACHO_S7_NS   // tuning / debugging override
@@ -63,6 +68,7 @@ struct S7Args {
   int64_t* z_pos;
   int32_t* z_crd;
   V* z_val;
+  double* partial;                      // kS7InterSum: [P] per-partition sums of products
 };
 
 template <typename V, int K>
@@ -89,6 +95,7 @@ struct S7Smem {
   uint16_t src2[K >= 4 ? kS7Slots + 16 : 1];
   int32_t ML[kS7LMax + 1];        // merged position of each owned row's first entry
   int32_t wred[kS7Compute / 32];
+  double wsum[kS7Compute / 32];
   int64_t run_off;
   int64_t excl[S7Cfg<V, K>::NS];     // emission -> compute: exclusive prefix of the stage's job
   int32_t excl_ok[S7Cfg<V, K>::NS];  // ... once resolved (reset by the emission after the job)
@@ -115,7 +122,7 @@ __device__ __forceinline__ void s7_wait_sleep(uint64_t* bar, uint32_t parity, un
 }
 
 // ------------------------------------------------------------------ producer warp
-template <typename V, int K>
+template <typename V, int K, int OP>
 __device__ __forceinline__ void s7_produce(const S7Args<V>& a, S7Smem<V, K>& sh) {
   constexpr int NS = S7Cfg<V, K>::NS;
   const int lane = threadIdx.x & 31;
@@ -135,7 +142,7 @@ __device__ __forceinline__ void s7_produce(const S7Args<V>& a, S7Smem<V, K>& sh)
         ps_o = a.parts.pos[t * K + lane];
         pe_o = a.parts.pos[(t + 1) * K + lane];
       }
-      if (t == 0 && lane == 0) a.z_pos[0] = 0;
+      if (t == 0 && lane == 0 && a.z_pos) a.z_pos[0] = 0;
     }
   };
   // one job: (sub-)tile rows (a0, a0 + lrows], operand o's range [so, eo) held by lane o
@@ -252,7 +259,7 @@ __device__ __forceinline__ void s7_produce(const S7Args<V>& a, S7Smem<V, K>& sh)
       continue;
     }
     const int nsub = (int)((L + lmax) / lmax);
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < (OP == kS7InterSum ? 1 : 2); ++pass) {
       for (int j = 0; j < nsub; ++j) {
         const int64_t a0 = row0 + (int64_t)j * lmax;
         const int lrows = (int)(j < nsub - 1 ? lmax : L - (int64_t)j * lmax);
@@ -269,7 +276,7 @@ __device__ __forceinline__ void s7_produce(const S7Args<V>& a, S7Smem<V, K>& sh)
 }
 
 // ------------------------------------------------------------------ emission warp
-template <typename V, int K>
+template <typename V, int K, int OP>
 __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
   constexpr int NS = S7Cfg<V, K>::NS;
   const int lane = threadIdx.x & 31;
@@ -284,7 +291,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
     const int64_t t = g.tile;
     const int mode = g.mode;
     int64_t excl = 0;
-    if (t > 0 && mode == 1) {
+    if (OP != kS7InterSum && t > 0 && mode == 1) {
       S7_T0();
       excl = s5_lookback(a.state, t);
       if (lane == 0) S7_ACC(2);   // emission: look-back
@@ -301,7 +308,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
     }
     if (lane == 0) sh.excl_ok[s] = 0;
     if (t < 0) break;
-    if (mode != 0) {
+    if (OP != kS7InterSum && mode != 0) {
       const int total = g.total, lrows = g.lrows;
       const int64_t a0 = g.a0;
       int64_t off;
@@ -342,7 +349,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
 template <int K>
 __host__ __device__ constexpr int s7_bw() { return (3 * (kS7Slots + 16) / 2 - 8) / (K + 2); }
 
-template <typename V, int K>
+template <typename V, int K, int OP>
 __device__ __forceinline__ int s7_bitmap(S7Stage<V, K>& g, S7Smem<V, K>& sh, int cmin, int nw, int S, bool emit) {
   const int tid = threadIdx.x;
   uint32_t* bm = sh.key1;              // [K][nw] operand bitmaps, then U[nw] union, pre[nw + 1]
@@ -394,9 +401,9 @@ __device__ __forceinline__ int s7_bitmap(S7Stage<V, K>& g, S7Smem<V, K>& sh, int
   const int w0 = tid * wpt;
   int cnt = 0;
   for (int w = w0; w < w0 + wpt && w < nw; ++w) {
-    uint32_t u = 0;
+    uint32_t u = OP == kS7Union ? 0u : ~0u;
 #pragma unroll
-    for (int q = 0; q < K; ++q) u |= bm[q * nw + w];
+    for (int q = 0; q < K; ++q) u = OP == kS7Union ? (u | bm[q * nw + w]) : (u & bm[q * nw + w]);
     U[w] = u;
     cnt += __popc(u);
   }
@@ -416,15 +423,25 @@ __device__ __forceinline__ int s7_bitmap(S7Stage<V, K>& g, S7Smem<V, K>& sh, int
       if (oo[i] == o) {
         const int w = (int)(c[i] >> 5);
         const uint32_t bit = c[i] & 31;
-        const int idx = (int)pre[w] + __popc(U[w] & ((1u << bit) - 1u));
-        uint32_t lower = 0;
+        const uint32_t uw = U[w];
+        const int idx = (int)pre[w] + __popc(uw & ((1u << bit) - 1u));
+        if (OP == kS7Union) {
+          uint32_t lower = 0;
 #pragma unroll
-        for (int q = 0; q < K; ++q) if (q < o) lower |= bm[q * nw + w];
-        if ((lower >> bit) & 1u) {
-          g.val[idx] = g.val[idx] + v[i];
-        } else {
-          g.key[idx] = c[i] + (uint32_t)cmin;
-          g.val[idx] = v[i];
+          for (int q = 0; q < K; ++q) if (q < o) lower |= bm[q * nw + w];
+          if ((lower >> bit) & 1u) {
+            g.val[idx] = g.val[idx] + v[i];
+          } else {
+            g.key[idx] = c[i] + (uint32_t)cmin;
+            g.val[idx] = v[i];
+          }
+        } else if ((uw >> bit) & 1u) {   // in every operand: the product, left to right
+          if (o == 0) {
+            g.key[idx] = c[i] + (uint32_t)cmin;
+            g.val[idx] = v[i];
+          } else {
+            g.val[idx] = g.val[idx] * v[i];
+          }
         }
       }
     }
@@ -434,12 +451,13 @@ __device__ __forceinline__ int s7_bitmap(S7Stage<V, K>& g, S7Smem<V, K>& sh, int
 }
 
 // ------------------------------------------------------------------ compute warps
-template <typename V, int K>
+template <typename V, int K, int OP>
 __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh) {
   constexpr int NS = S7Cfg<V, K>::NS;
   const int tid = threadIdx.x;
   const int P = a.parts.P;
   int64_t cnt_total = 0, run_off = 0;
+  double sum_run = 0.0;   // kS7InterSum: the current partition's sum over its sub-tiles (thread 0)
   for (int njob = 0;; ++njob) {
     const int s = njob % NS;
     {
@@ -479,7 +497,7 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
     const long long _tc = clock64();
 #endif
     if (bmp) {
-      total = s7_bitmap<V, K>(g, sh, cmin, nw, S, mode != 0);
+      total = s7_bitmap<V, K, OP>(g, sh, cmin, nw, S, mode != 0 || OP == kS7InterSum);
     } else {
       // ---- partition-local row of every slot (multi-row jobs only), keys in place, run sentinels
       if (lrows > 0) {
@@ -568,6 +586,7 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
         uint32_t xk = X[i], yk = Y[jj];
         bool own = false;
         V acc = V(0);
+        int rl = 0;   // operands storing the current key (the run length)
   #pragma unroll
         for (int v = 0; v < kS5VT; ++v) {
           uint32_t key;
@@ -575,26 +594,29 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
           s5_step<XSRC>(X, XS, xs0, Y, ys0, i, jj, xk, yk, key, slot);
           const bool valid = d + v < n;
           const bool start = valid && key != pk;
-          if (v > 0 && own && (start || !valid) && d + v - 1 < n) em |= 1u << (v - 1);
+          // a run ends: one union entry; an intersection entry only if every operand stores the key
+          if (v > 0 && own && (start || !valid) && d + v - 1 < n && (OP == kS7Union || rl == K)) em |= 1u << (v - 1);
           own = own || start;
           if (own && valid) {
             const V x = g.val[slot];
-            acc = start ? x : acc + x;
+            acc = start ? x : (OP == kS7Union ? acc + x : acc * x);
+            rl = start ? 1 : rl + 1;
           }
           res[v] = acc;
           col[v] = key & cmask;
           pk = key;
         }
         if (own && d + kS5VT <= n) {   // the last run may continue past this thread's items
-          em |= 1u << (kS5VT - 1);
   #pragma unroll
           for (int r = 0; r < K - 1; ++r) {
             if (d + kS5VT + r >= n || (xk <= yk ? xk : yk) != pk) break;
             uint32_t key;
             int slot;
             s5_step<XSRC>(X, XS, xs0, Y, ys0, i, jj, xk, yk, key, slot);
-            acc = acc + g.val[slot];
+            acc = OP == kS7Union ? acc + g.val[slot] : acc * g.val[slot];
+            ++rl;
           }
+          if (OP == kS7Union || rl == K) em |= 1u << (kS5VT - 1);
           res[kS5VT - 1] = acc;
         }
       }
@@ -604,6 +626,33 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
     if (tid == 0) atomicAdd(a.state + a.parts.P + 2 + (bmp ? 4 : 5), (unsigned long long)(clock64() - _tc));
     if (tid == 0) atomicAdd(a.state + a.parts.P + 2 + (bmp ? 6 : 7), 1ull);
 #endif
+    if (OP == kS7InterSum) {   // the partition's sum of products (deterministic order), no output
+      double ps = 0.0;
+      if (bmp) {
+        s6_sync();   // the last operand phase's products
+        for (int q = tid; q < total; q += kS7Compute) ps += (double)g.val[q];
+      } else {
+#pragma unroll
+        for (int v = 0; v < kS5VT; ++v) if (em & (1u << v)) ps += (double)res[v];
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) ps += __shfl_xor_sync(kFull, ps, o2);
+      if ((tid & 31) == 0) sh.wsum[tid >> 5] = ps;
+      s6_sync();
+      if (tid == 0) {
+        double js = 0.0;
+        for (int w = 0; w < kS7Compute / 32; ++w) js += sh.wsum[w];
+        sum_run += js;
+        if (mode == 1 || last) {
+          a.partial[t] = sum_run;
+          sum_run = 0.0;
+        }
+        g.total = total;
+      }
+      s6_sync();
+      if (tid == 0) mbar_arrive(&sh.done[s]);
+      continue;
+    }
     if (mode == 0) {   // count a sub-tile; after the last one: publish, look back, known offset
       cnt_total += total;
       if (last) {
@@ -662,7 +711,7 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
   }
 }
 
-template <typename V, int K>
+template <typename V, int K, int OP>
 __global__ void __launch_bounds__(kS7Threads, S7Cfg<V, K>::MINB) spadd7_kernel(const S7Args<V> a) {
   extern __shared__ __align__(128) unsigned char s7_raw[];
   S7Smem<V, K>& sh = *reinterpret_cast<S7Smem<V, K>*>(s7_raw);
@@ -678,9 +727,26 @@ __global__ void __launch_bounds__(kS7Threads, S7Cfg<V, K>::MINB) spadd7_kernel(c
   }
   __syncthreads();
   const int w = threadIdx.x >> 5;
-  if (w == kS7Compute / 32) s7_produce<V, K>(a, sh);
-  else if (w == kS7Compute / 32 + 1) s7_emit<V, K>(a, sh);
-  else s7_compute<V, K>(a, sh);
+  if (w == kS7Compute / 32) s7_produce<V, K, OP>(a, sh);
+  else if (w == kS7Compute / 32 + 1) s7_emit<V, K, OP>(a, sh);
+  else s7_compute<V, K, OP>(a, sh);
+}
+
+// Sum of the per-partition partials in a fixed order (one CTA): the inner product's final reduction.
+__global__ void __launch_bounds__(1024) s7_sum_partials_kernel(const double* __restrict__ partial, int64_t P,
+                                                               double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t p = threadIdx.x; p < P; p += blockDim.x) s += partial[p];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
 }
 
 }  // namespace nacho
