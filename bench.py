@@ -572,6 +572,43 @@ def bench_spmv(N, W, torch, name, scale, K, Wu, timer, column_kind=None):
                 dtype="f32" if vs == 4 else "f64", wl=wl)
 
 
+def bench_intersection(N, W, torch, scale, K, Wu, timer):
+    """C2's three operands coiterated as an intersection: partition + Hadamard
+    A (.) B (.) C (nacho_hadamard_k), and the intersect-reduce inner product (nacho_inner_k)."""
+    wl = W.build("c2", scale, device="cuda")
+    ops = wl.ops
+    k = len(ops)
+    P = N.auto_partitions(ops, "spadd")
+    parts = N.Parts(P, k, "cuda")
+    cap = min(A.nnz for A in ops)
+    z_pos = torch.empty(ops[0].nrows + 1, dtype=torch.int64, device="cuda")
+    z_crd = torch.empty(cap, dtype=torch.int32, device="cuda")
+    z_val = torch.empty(cap, dtype=torch.float32, device="cuda")
+    ws = torch.empty(N.lib.nacho_inner_k_workspace_size(N._matrices(ops), k, P), dtype=torch.uint8, device="cuda")
+    res = torch.empty(1, dtype=torch.float64, device="cuda")
+
+    def step(timed=False):
+        m = [ev(torch)] if timed else None
+        N.partition(ops, P, out=parts)
+        if timed:
+            m.append(ev(torch))
+        N.hadamard_k(ops, parts, z_pos, z_crd, z_val, ws=ws)
+        if timed:
+            m.append(ev(torch))
+        N.inner_k(ops, parts, out=res, ws=ws)
+        if timed:
+            m.append(ev(torch))
+        return m
+    times, sec = timer.run(step, K, Wu, ["partition", "hadamard", "inner"])
+    nnz_z = int(z_pos[-1].item())
+    M = ops[0].nrows
+    pos_arrays = {A.pos.data_ptr() for A in ops}
+    read = sum(A.nnz * 8 for A in ops) + len(pos_arrays) * (M + 1) * 8
+    return dict(work=sum(A.nnz for A in ops), times=times, sec=sec, algo_step=2 * read + nnz_z * 8 + (M + 1) * 8,
+                kernel_bytes={"hadamard": read + nnz_z * 8 + (M + 1) * 8, "inner": read,
+                              "partition": (P + 1) * (8 * k + 28)}, P=P, dtype="f32", wl=wl, nnz_z=nnz_z)
+
+
 def bench_spmm(N, W, torch, scale, K, Wu, timer):
     wl = W.build("c4", scale, device="cuda")
     A = wl.ops[0]
@@ -840,6 +877,7 @@ def main():
         for name, fn in [("c5_spmv_csr_f32", lambda: bench_spmv(N, W, torch, "c5", args.scale, 10, 3, timer)),
                          ("c3_spmv_dcsr_f32", lambda: bench_spmv(N, W, torch, "c3", args.scale, 10, 3, timer)),
                          ("c4_spmm_f32_nb64", lambda: bench_spmm(N, W, torch, args.scale, 5, 2, timer)),
+                         ("c2_hadamard3_and_inner", lambda: bench_intersection(N, W, torch, args.scale, 10, 3, timer)),
                          ("c1_spmv_csr_f64_P8", lambda: bench_spmv(N, W, torch, "c1", 1.0, 20, 3, timer))]:
             try:
                 rr = fn()
