@@ -20,6 +20,7 @@
 #include "spmm.cuh"
 #include "spmv.cuh"
 #include "spmv3.cuh"
+#include "spmv7.cuh"
 
 using namespace nacho;
 
@@ -76,7 +77,17 @@ nacho_status smem_optin(F kern, size_t smem, std::atomic<uint64_t>& done, const 
   return NACHO_SUCCESS;
 }
 
-int64_t spmv_tile(int dtype) { return dtype == NACHO_F64 ? sv3_tile<double>() : sv3_tile<float>(); }  // = spmv3 tile
+int spmv_impl() {   // 3: one tile per CTA (spmv3.cuh, default); 7: the experimental pipelined spmv7.cuh
+  static const int impl = [] {
+    const char* e = getenv("NACHO_SPMV_IMPL");
+    return e && e[0] == '7' ? 7 : 3;
+  }();
+  return impl;
+}
+int64_t spmv_tile(int dtype) {   // positions per tile of the SpMV kernel in use (= the auto partition size)
+  if (spmv_impl() == 7) return dtype == NACHO_F64 ? sv7_tile<double>() : sv7_tile<float>();
+  return dtype == NACHO_F64 ? sv3_tile<double>() : sv3_tile<float>();
+}
 
 nacho_status check_matrix(const nacho_matrix* A, const char* name) {
   if (!A) return fail(NACHO_ERR_INVALID_ARG, "%s: null descriptor", name);
@@ -186,7 +197,7 @@ nacho_status launch_partition(const nacho_matrix* ops, int32_t k, const PartsArg
 // Carries of an SpMV over P partitions made by nacho_partition (work <= ceil(nnz / P)): one per
 // tile-sized chunk.
 int64_t spmv_carry_cap(const nacho_matrix* A, int64_t P) {
-  const int64_t tile = A->dtype == NACHO_F64 ? sv3_tile<double>() : sv3_tile<float>();
+  const int64_t tile = spmv_tile(A->dtype);
   const int64_t w = (A->nnz + P - 1) / P;
   return P * (w <= tile ? 1 : (w + tile - 1) / tile);
 }
@@ -196,6 +207,22 @@ int32_t auto_p(int64_t work, int64_t tile) {
   if (P < 1) P = 1;
   if (P > INT32_MAX - 1) P = INT32_MAX - 1;
   return (int32_t)P;
+}
+
+template <typename T, bool DY>
+nacho_status launch_spmv7(const SpmvArgs<T>& a, cudaStream_t st) {
+  auto kern = spmv7_kernel<T, DY>;
+  const size_t smem = sizeof(Sv7Smem<T>);
+  static std::atomic<uint64_t> done{0};   // per instantiation: the opt-in is per kernel and device
+  NACHO_TRY(smem_optin(kern, smem, done, "spmv7_kernel"));
+  int dev = 0, sms = 0, per = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kSv7Threads, smem) != cudaSuccess || per < 1)
+    return fail(NACHO_ERR_CUDA, "spmv7 occupancy query");
+  const int64_t grid = std::min<int64_t>(a.P, (int64_t)sms * per);
+  kern<<<(unsigned)grid, kSv7Threads, smem, st>>>(a, (int64_t)a.P);
+  return launched("spmv7_kernel");
 }
 
 template <typename T>
@@ -210,8 +237,12 @@ nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, 
   a.dense_y = (A->format == NACHO_DCSR && dense_y) ? 1 : 0;
   a.ppos = pa.pos; a.prow = pa.row_pos;
   // partitions larger than a tile run as tile-sized chunks (one CTA each, spmv3.cuh)
-  const int64_t maxpart = max_part_work(A, 1, pa, sv3_tile<T>(), st);
-  const int64_t chunks = maxpart <= sv3_tile<T>() ? 1 : (maxpart + sv3_tile<T>() - 1) / sv3_tile<T>();
+  const bool aligned = reinterpret_cast<uintptr_t>(A->crd) % 16 == 0 && reinterpret_cast<uintptr_t>(A->val) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(A->pos) % 16 == 0;
+  const bool use7 = spmv_impl() == 7 && aligned && A->nnz > 0;
+  const int64_t tile = use7 ? sv7_tile<T>() : sv3_tile<T>();
+  const int64_t maxpart = max_part_work(A, 1, pa, tile, st);
+  const int64_t chunks = maxpart <= tile ? 1 : (maxpart + tile - 1) / tile;
   if (int64_t(pa.P) * chunks > carry_cap)
     return fail(NACHO_ERR_WORKSPACE, "partitions of up to %lld positions need %lld carries, workspace holds %lld",
                 (long long)maxpart, (long long)(int64_t(pa.P) * chunks), (long long)carry_cap);
@@ -222,9 +253,13 @@ nacho_status run_spmv(const nacho_matrix* A, const PartsArg& pa, const void* x, 
   if (a.dense_y) {
     if (cudaMemsetAsync(y, 0, sizeof(T) * A->nrows, st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "memset y");
   }
-  if (a.dense_y) spmv3_kernel<T, true><<<(unsigned)a.P, kSv3Threads, 0, st>>>(a);
-  else spmv3_kernel<T, false><<<(unsigned)a.P, kSv3Threads, 0, st>>>(a);
-  NACHO_TRY(launched("spmv3_kernel"));
+  if (use7) {   // persistent, bulk-copy pipelined (spmv7.cuh)
+    NACHO_TRY((a.dense_y ? launch_spmv7<T, true>(a, st) : launch_spmv7<T, false>(a, st)));
+  } else {
+    if (a.dense_y) spmv3_kernel<T, true><<<(unsigned)a.P, kSv3Threads, 0, st>>>(a);
+    else spmv3_kernel<T, false><<<(unsigned)a.P, kSv3Threads, 0, st>>>(a);
+    NACHO_TRY(launched("spmv3_kernel"));
+  }
   const int64_t warps = (int64_t(a.P) + 31) / 32;
   spmv_fixup_kernel<T><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
   return launched("spmv_fixup_kernel");

@@ -31,7 +31,7 @@ template <> struct Sv3Cfg<double> { static constexpr int V = 8, MINB = 3; };
 
 // positions per partition
 template <typename T>
-constexpr int sv3_tile() { return kSv3Threads * Sv3Cfg<T>::V; }
+__host__ __device__ constexpr int sv3_tile() { return kSv3Threads * Sv3Cfg<T>::V; }
 
 template <typename T>
 struct KVl { int k; T v; };
@@ -74,7 +74,15 @@ __device__ __forceinline__ FV<T> fv_op(FV<T> a, FV<T> b) { return FV<T>{a.f | b.
 
 // Steps 2-5 of a tile (after the products are in sprod and the row ends in send, and a barrier):
 // row-start marks, segmented scan, row sums, carry.  Ends with every smem read done (barrier).
-template <typename T, int V, bool DY>
+// BAR 0: __syncthreads (one tile per CTA); 1: named barrier 1 of the kSv3Threads compute threads
+// (spmv7.cuh's persistent CTAs, whose producer warp does not take part).
+template <int BAR>
+__device__ __forceinline__ void sv3_sync() {
+  if constexpr (BAR == 0) __syncthreads();
+  else asm volatile("bar.sync 1, %0;" ::"r"(kSv3Threads) : "memory");
+}
+
+template <typename T, int V, bool DY, int BAR = 0>
 __device__ __forceinline__ void sv3_tail(const SpmvArgs<T>& a, int64_t p, int64_t s, int n, int64_t rp0, int64_t rpE,
                                          int lim_r, bool smem_rows, const int32_t* send, T* sprod, uint8_t* mark,
                                          FV<T>* s_wagg, T* s_cin, int32_t* s_ffl) {
@@ -86,7 +94,7 @@ __device__ __forceinline__ void sv3_tail(const SpmvArgs<T>& a, int64_t p, int64_
     const int q = row_end(r);
     if (q < n) mark[q] = 1;
   }
-  __syncthreads();
+  sv3_sync<BAR>();
 
   // 3. segmented inclusive scan over my V consecutive items (in place), then across threads
   const int j0 = tid * V;
@@ -133,7 +141,7 @@ __device__ __forceinline__ void sv3_tail(const SpmvArgs<T>& a, int64_t p, int64_
     if (lane >= dd) inc = fv_op(u, inc);
   }
   if (lane == 31) s_wagg[w] = inc;
-  __syncthreads();
+  sv3_sync<BAR>();
   FV<T> pre = FV<T>{0, T(0)};
   for (int ww = 0; ww < w; ++ww) pre = fv_op(pre, s_wagg[ww]);
   FV<T> excl;
@@ -142,7 +150,7 @@ __device__ __forceinline__ void sv3_tail(const SpmvArgs<T>& a, int64_t p, int64_
   excl = (lane == 0) ? pre : fv_op(pre, excl);
   s_cin[tid] = excl.v;
   s_ffl[tid] = ffl;
-  __syncthreads();
+  sv3_sync<BAR>();
 
   // 4. row sums: the segmented prefix at the row's last item (+ the carry-in when that item lies in
   //    its thread's leading run); empty rows are 0.  One thread per owned row.
