@@ -568,8 +568,13 @@ def bench_spmv(N, W, torch, name, scale, K, Wu, timer, column_kind=None):
     else:
         distinct = int(torch.unique(A.crd).numel())
         algo = nnz * (4 + vs) + A.nouter * (4 + 8) + distinct * vs + A.nouter * vs
-    return dict(work=nnz, times=times, sec=sec, algo_step=algo, kernel_bytes={"spmv+fixup": algo}, P=P,
-                dtype="f32" if vs == 4 else "f64", wl=wl)
+    out = dict(work=nnz, times=times, sec=sec, algo_step=algo, kernel_bytes={"spmv+fixup": algo}, P=P,
+               dtype="f32" if vs == 4 else "f64", wl=wl)
+    if A.format != "csr":
+        # gather-granularity bound (uniform random columns over a 400 MB x: every gather moves a
+        # 32-byte DRAM sector): crd + val once, the row level, one sector per nonzero
+        out["gather_bytes"] = nnz * (4 + vs) + A.nouter * 16 + nnz * 32
+    return out
 
 
 def bench_intersection(N, W, torch, scale, K, Wu, timer):
@@ -882,7 +887,10 @@ def main():
             try:
                 rr = fn()
                 s, d, _, ach = summarize(rr, peak)
-                kern[name] = {"gnnz_s": s["gnnz_s"], "ms_per_step": s["ms_per_step"],
+                if rr.get("gather_bytes"):
+                    kern.setdefault(name, {})["gather_bound_frac"] = rr["gather_bytes"] / (
+                        statistics.mean(rr["sec"][d]) * 1e-3) / 1e9 / peak
+                kern[name] = {**kern.get(name, {}), "gnnz_s": s["gnnz_s"], "ms_per_step": s["ms_per_step"],
                               "step_hbm_frac": s["step_hbm_frac"], "dominant": d,
                               "dominant_hbm_frac": ach / peak, "dominant_frac_nominal_8tbs": ach / NOMINAL_HBM_GBS, "sections_ms": s["sections_ms"], "P": s["P"],
                               "traffic": traffic_table().get(f"{name.split('_')[0]}:{d}")}

@@ -132,6 +132,9 @@ OpsArg make_ops(const nacho_matrix* ops, int32_t k) {
     a.op[o].nouter = ops[o].nouter;
     a.op[o].nnz = ops[o].nnz;
   }
+  a.pos_shared = 1;
+  for (int o = 1; o < k; ++o)
+    if (ops[o].pos != ops[0].pos) a.pos_shared = 0;
   return a;
 }
 

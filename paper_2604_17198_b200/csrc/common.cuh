@@ -28,6 +28,7 @@ struct OpsArg {
   int32_t k;
   int32_t dtype;
   int64_t nrows, ncols;
+  int32_t pos_shared;   // every operand's pos is one array (same row profile): C_i(x) = k * pos[x]
 };
 
 // Partition record (device pointers), see nacho_parts.
@@ -299,6 +300,7 @@ __device__ __forceinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t 
   const int k = a.k;
   // ---- level i
   auto outer_ok = [&](int64_t x) {
+    if (a.pos_shared) return (int64_t)k * ldg(a.op[0].pos + x) <= Q;   // one load instead of k
     int64_t s = 0;
 #pragma unroll
     for (int o = 0; o < KM; ++o) if (o < k) s += ldg(a.op[o].pos + x);
@@ -319,8 +321,8 @@ __device__ __forceinline__ Boundary warp_find_boundary(const OpsArg& a, int64_t 
 #pragma unroll
   for (int o = 0; o < KM; ++o) {
     if (o < k) {
-      lo[o] = ldg(a.op[o].pos + x);
-      hi[o] = ldg(a.op[o].pos + x + 1);
+      lo[o] = ldg((a.pos_shared ? a.op[0].pos : a.op[o].pos) + x);
+      hi[o] = ldg((a.pos_shared ? a.op[0].pos : a.op[o].pos) + x + 1);
       R -= lo[o];
     }
   }

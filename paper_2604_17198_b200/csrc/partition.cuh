@@ -11,7 +11,10 @@ namespace nacho {
 template <int WARPS, int KM>
 // Boundaries p0 .. p0 + out.P of the Ptot-partition go to out[0 .. out.P] (a whole partition: p0 = 0,
 // Ptot = out.P; a device slice otherwise).
-__global__ void __launch_bounds__(WARPS * 32) partition_kernel(const __grid_constant__ OpsArg a, PartsArg out, int64_t qstar,
+#ifndef NACHO_PART_MINB   // tuning override: CTAs per SM the register allocation must allow
+#define NACHO_PART_MINB 8   // 64 registers: 50 % occupancy (47 vs 51 us on C2; a few spilled bytes)
+#endif
+__global__ void __launch_bounds__(WARPS * 32, NACHO_PART_MINB) partition_kernel(const __grid_constant__ OpsArg a, PartsArg out, int64_t qstar,
                                                                int64_t Ptot, int64_t p0) {
   const int64_t i = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (i > out.P) return;  // warp-uniform

@@ -303,7 +303,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
     }
     {
       S7_T0();
-      s7_wait_sleep(&sh.done[s], ph, 64);
+      s7_wait_sleep(&sh.done[s], ph, 256);
       if (lane == 0) S7_ACC(1);   // emission: waiting for a computed stage
     }
     if (lane == 0) sh.excl_ok[s] = 0;
@@ -462,7 +462,7 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
     const int s = njob % NS;
     {
       S7_T0();
-      s7_wait_sleep(&sh.full[s], (uint32_t)(njob / NS) & 1u, 32);
+      s7_wait_sleep(&sh.full[s], (uint32_t)(njob / NS) & 1u, 128);
       if (tid == 0) S7_ACC(3);   // compute: waiting for a loaded stage
     }
     S7Stage<V, K>& g = sh.st[s];

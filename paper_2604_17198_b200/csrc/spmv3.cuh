@@ -1,6 +1,6 @@
-// spmv3.cuh -- partitioned CSR / DCSR SpMV: one CTA per partition of at
-// most sv3_tile<T>() positions (nacho_auto_partitions sizes P so; larger user partitions take
-// spmv_kernel's chunk loop).
+// spmv3.cuh -- partitioned CSR / DCSR SpMV: one CTA per tile of at most
+// sv3_tile<T>() positions (nacho_auto_partitions sizes P so that a partition is one tile; a larger
+// user partition runs as tile-sized chunks, one CTA each, cut in position space).
 //
 // Design (an HBM stream plus an x gather; no tensor cores).  Two limiters besides DRAM shape it:
 //   * the L1TEX wavefronts of the x gather: a warp-wide load costs one wavefront per distinct
