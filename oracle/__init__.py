@@ -62,6 +62,13 @@ def lib():
         L.oracle_hadamard_k.restype = ctypes.c_int64
         L.oracle_hadamard_counts.argtypes = [ctypes.c_int32, vp, vp, vp]
         L.oracle_inner_k.argtypes = [ctypes.c_int32, vp, vp]
+        i64 = ctypes.c_int64
+        L.oracle_dcsr_rows_intersect.argtypes = [ctypes.c_int32, vp, vp, vp, vp, i64]
+        L.oracle_dcsr_rows_intersect.restype = i64
+        L.oracle_exclusive_prefix.argtypes = [vp, i64, vp]
+        L.oracle_partition_remapped.argtypes = [ctypes.c_int32, vp, i64, vp, vp, i64, vp, ctypes.c_int32, vp]
+        L.oracle_dcsr_hadamard.argtypes = [ctypes.c_int32, vp, i64, vp, i64, vp, vp, vp, i64]
+        L.oracle_dcsr_hadamard.restype = i64
     return _lib
 
 
@@ -219,4 +226,63 @@ def inner_k(ops) -> float:
     if lib().oracle_inner_k(len(ops), arr, ctypes.byref(out)) != 0:
         raise ValueError("oracle_inner_k failed")
     return float(out.value)
+
+
+class Remap:
+    """Lines 2-4 of Listing emul-dcsr2-rewritten: surviving rows, T, T', outer positions ip[o][s]."""
+
+    def __init__(self, rows, T, Tp, ip):
+        self.rows, self.T, self.Tp, self.ip = rows, T, Tp, ip
+        self.S = len(rows)
+
+
+def dcsr_rows_intersect(ops) -> Remap:
+    arr, keep = _matrices(ops)
+    k = len(ops)
+    cap = max(1, min(int(A.nouter) for A in ops))
+    rows = np.zeros(cap, np.int64)
+    T = np.zeros(cap, np.int64)
+    ip = np.zeros(k * cap, np.int64)
+    S = lib().oracle_dcsr_rows_intersect(k, arr, _p(rows), _p(T), _p(ip), cap)
+    if S < 0:
+        raise ValueError("oracle_dcsr_rows_intersect failed (DCSR operands only)")
+    Tp = np.zeros(S + 1, np.int64)
+    lib().oracle_exclusive_prefix(_p(T), S, _p(Tp))
+    ipm = ip.reshape(k, cap)[:, :S].copy()
+    return Remap(rows[:S].copy(), T[:S].copy(), Tp, ipm)
+
+
+def _ip_flat(rm):
+    k = rm.ip.shape[0]
+    cap = max(1, rm.S)
+    flat = np.zeros(k * cap, np.int64)
+    for o in range(k):
+        flat[o * cap:o * cap + rm.S] = rm.ip[o]
+    return flat, cap
+
+
+def partition_remapped(ops, rm: Remap, P) -> Parts:
+    arr, keep = _matrices(ops)
+    out = Parts(P, len(ops))
+    flat, cap = _ip_flat(rm)
+    rows = np.ascontiguousarray(rm.rows, np.int64) if rm.S else np.zeros(1, np.int64)
+    s = out.c()
+    if lib().oracle_partition_remapped(len(ops), arr, rm.S, _p(rows), _p(flat), cap, _p(rm.Tp), P,
+                                       ctypes.byref(s)) != 0:
+        raise ValueError("oracle_partition_remapped failed")
+    return out
+
+
+def dcsr_hadamard(ops, rm: Remap):
+    """(z_outer, z_pos, z_crd, z_val): Z over the surviving rows (every one stored, R21)."""
+    arr, keep = _matrices(ops)
+    flat, cap = _ip_flat(rm)
+    zcap = max(1, min(int(A.crd.shape[0]) for A in ops))
+    z_pos = np.zeros(rm.S + 1, np.int64)
+    z_crd = np.zeros(zcap, np.int32)
+    z_val = np.zeros(zcap, dtype=ops[0].val.dtype)
+    n = lib().oracle_dcsr_hadamard(len(ops), arr, rm.S, _p(flat), cap, _p(z_pos), _p(z_crd), _p(z_val), zcap)
+    if n < 0:
+        raise ValueError("oracle_dcsr_hadamard failed")
+    return rm.rows.astype(np.int32), z_pos, z_crd[:n].copy(), z_val[:n].copy()
 

@@ -455,3 +455,153 @@ int oracle_inner_k(int32_t k, const or_matrix *ops, double *out) {
     return 0;
 }
 
+/* --------------------------------------------- recursive partitioning (Alg. 2) */
+/*
+ * The DCSR Hadamard product Z = A_0 (.) ... (.) A_{k-1} of Listing emul-dcsr2-cfir has an
+ * outer sparse intersection, so Alg. 2 remaps the row cost before partitioning.  These
+ * functions follow Listing emul-dcsr2-rewritten line by line:
+ *   line 2-3  while i <- rows(A_0) cap ... cap rows(A_{k-1}):  T[i] = C_j(N_j | i)
+ *             (C_j(N_j | i) = the non-zeros of row i over the operands, the nnz cost of P:1689),
+ *   line 4    T' = exclusive_prefix_sum(T),
+ *   line 5    C'_i(x_i) = T'[x_i]  (the remapped cost),
+ *   line 7-9  for i <- i_T:  while j <- cols(A_0[i]) cap ...:  Z[i, j] = prod_o A_o[i, j].
+ */
+
+/* Lines 2-3: the surviving rows (k-finger intersection of the outer levels, Listing 1's predicate)
+ * with T and every operand's outer position of the row.  rows / T / ip (ip[o * cap + s]) need
+ * capacity >= min_o nouter_o.  Returns S, the number of surviving rows, or -1. */
+int64_t oracle_dcsr_rows_intersect(int32_t k, const or_matrix *ops, int64_t *rows, int64_t *T, int64_t *ip,
+                                   int64_t cap) {
+    for (int32_t o = 0; o < k; o++) if (ops[o].format != OR_DCSR) return -1;
+    int64_t *q = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t S = 0;
+    for (;;) {
+        int inside = 1;
+        for (int32_t o = 0; o < k; o++) if (q[o] >= ops[o].nouter) inside = 0;
+        if (!inside) break;
+        int64_t r = ops[0].outer_crd[q[0]];
+        for (int32_t o = 1; o < k; o++) if (ops[o].outer_crd[q[o]] < r) r = ops[o].outer_crd[q[o]];
+        int all = 1;
+        for (int32_t o = 0; o < k; o++) if (ops[o].outer_crd[q[o]] != r) all = 0;
+        if (all) {
+            if (S >= cap) { free(q); return -1; }
+            int64_t t = 0;
+            for (int32_t o = 0; o < k; o++) {
+                t += ops[o].pos[q[o] + 1] - ops[o].pos[q[o]];
+                ip[(int64_t)o * cap + S] = q[o];
+            }
+            rows[S] = r;
+            T[S] = t;
+            S++;
+        }
+        for (int32_t o = 0; o < k; o++) if (ops[o].outer_crd[q[o]] == r) q[o]++;
+    }
+    free(q);
+    return S;
+}
+
+/* Line 4: T' = exclusive prefix sum of T (S + 1 entries, T'[S] = the remapped total cost). */
+void oracle_exclusive_prefix(const int64_t *T, int64_t S, int64_t *Tp) {
+    int64_t acc = 0;
+    for (int64_t s = 0; s < S; s++) { Tp[s] = acc; acc += T[s]; }
+    Tp[S] = acc;
+}
+
+/*
+ * Line 5-6: partition the remapped loop nest (i' over the surviving rows, j over the row's columns)
+ * with C'_i = T' and the inner nnz cost -- the plain definition of oracle_partition_rank applied to
+ * the remapped space: Q_p = floor(p * T'[S] / P) (R4), b_p = the coordinate of entry number Q_p of
+ * the lexicographic multiset of the surviving rows' entries (ties between operands irrelevant).
+ * row_pos = i' (index of the surviving row), row = rows[i'], col, pos[o] = absolute position in crd_o
+ * of operand o's first entry at or after b_p within row i'.  b_0: i' = 0, col 0, pos[o] = start of
+ * row 0's segment; b_P (and Q_p >= T'[S]): i' = S, row = nrows, col 0, pos[o] = end of the last
+ * surviving row's segment (0 when S = 0).
+ */
+int oracle_partition_remapped(int32_t k, const or_matrix *ops, int64_t S, const int64_t *rows, const int64_t *ip,
+                              int64_t cap, const int64_t *Tp, int32_t P, or_parts *out) {
+    if (k < 1 || P < 1) return 1;
+    oracle_queries(Tp[S], P, out->query);
+    for (int32_t p = 0; p <= P; p++) {
+        const int64_t Q = out->query[p];
+        if (p == 0 && S > 0) {                    /* origin (R1): the first surviving row, column 0 */
+            out->row[p] = rows[0]; out->row_pos[p] = 0; out->col[p] = 0;
+            for (int32_t o = 0; o < k; o++) out->pos[(int64_t)p * k + o] = ops[o].pos[ip[(int64_t)o * cap]];
+            continue;
+        }
+        if (p == P || Q >= Tp[S] || S == 0) {   /* end */
+            out->row[p] = ops[0].nrows; out->row_pos[p] = S; out->col[p] = 0;
+            for (int32_t o = 0; o < k; o++)
+                out->pos[(int64_t)p * k + o] = S > 0 ? ops[o].pos[ip[(int64_t)o * cap + S - 1] + 1] : 0;
+            continue;
+        }
+        /* the surviving row holding entry Q: highest s with T'[s] <= Q */
+        int64_t s = 0;
+        while (s + 1 < S && Tp[s + 1] <= Q) s++;
+        int64_t R = Q - Tp[s];            /* entry number R of row s's merged multiset */
+        int64_t *q = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+        for (int32_t o = 0; o < k; o++) q[o] = ops[o].pos[ip[(int64_t)o * cap + s]];
+        int64_t c = 0, col = 0;
+        for (;;) {                         /* k-finger union merge of row s until entry R */
+            int64_t j = -1;
+            for (int32_t o = 0; o < k; o++) {
+                const int64_t e = ops[o].pos[ip[(int64_t)o * cap + s] + 1];
+                if (q[o] < e && (j < 0 || ops[o].crd[q[o]] < j)) j = ops[o].crd[q[o]];
+            }
+            int64_t g = 0;
+            for (int32_t o = 0; o < k; o++) {
+                const int64_t e = ops[o].pos[ip[(int64_t)o * cap + s] + 1];
+                if (q[o] < e && ops[o].crd[q[o]] == j) g++;
+            }
+            if (R < c + g) { col = j; break; }
+            for (int32_t o = 0; o < k; o++) {
+                const int64_t e = ops[o].pos[ip[(int64_t)o * cap + s] + 1];
+                if (q[o] < e && ops[o].crd[q[o]] == j) q[o]++;
+            }
+            c += g;
+        }
+        out->row[p] = rows[s]; out->row_pos[p] = s; out->col[p] = (int32_t)col;
+        for (int32_t o = 0; o < k; o++) out->pos[(int64_t)p * k + o] = q[o];
+        free(q);
+    }
+    return 0;
+}
+
+/* Lines 7-9: Z over the surviving rows (DCSR: z_outer = the surviving rows, every one stored, with
+ * possibly empty segments -- reading R21), values the product in operand order (R17).  Returns nnz_Z. */
+int64_t oracle_dcsr_hadamard(int32_t k, const or_matrix *ops, int64_t S, const int64_t *ip, int64_t cap,
+                             int64_t *z_pos, int32_t *z_crd, void *z_val, int64_t zcap) {
+    const int f64 = ops[0].dtype == OR_F64;
+    int64_t *q = (int64_t *)malloc(sizeof(int64_t) * (size_t)k);
+    int64_t nz = 0;
+    z_pos[0] = 0;
+    for (int64_t s = 0; s < S; s++) {
+        for (int32_t o = 0; o < k; o++) q[o] = ops[o].pos[ip[(int64_t)o * cap + s]];
+        for (;;) {
+            int inside = 1;
+            for (int32_t o = 0; o < k; o++) if (q[o] >= ops[o].pos[ip[(int64_t)o * cap + s] + 1]) inside = 0;
+            if (!inside) break;
+            int64_t j = ops[0].crd[q[0]];
+            for (int32_t o = 1; o < k; o++) if (ops[o].crd[q[o]] < j) j = ops[o].crd[q[o]];
+            int all = 1;
+            for (int32_t o = 0; o < k; o++) if (ops[o].crd[q[o]] != j) all = 0;
+            if (all) {
+                if (nz >= zcap) { free(q); return -1; }
+                if (f64) {
+                    double v = ((const double *)ops[0].val)[q[0]];
+                    for (int32_t o = 1; o < k; o++) v = v * ((const double *)ops[o].val)[q[o]];
+                    ((double *)z_val)[nz] = v;
+                } else {
+                    float v = ((const float *)ops[0].val)[q[0]];
+                    for (int32_t o = 1; o < k; o++) v = v * ((const float *)ops[o].val)[q[o]];
+                    ((float *)z_val)[nz] = v;
+                }
+                z_crd[nz++] = (int32_t)j;
+            }
+            for (int32_t o = 0; o < k; o++) if (ops[o].crd[q[o]] == j) q[o]++;
+        }
+        z_pos[s + 1] = nz;
+    }
+    free(q);
+    return nz;
+}
+

@@ -80,6 +80,19 @@ int     oracle_hadamard_counts(int32_t k, const or_matrix *ops, const or_parts *
 /* s = sum over the intersection of the products (wide accumulation, rounded once to double). */
 int     oracle_inner_k(int32_t k, const or_matrix *ops, double *out);
 
+/* Recursive partitioning (Alg. 2) of the DCSR Hadamard product, Listing emul-dcsr2-rewritten: */
+/* lines 2-3: surviving rows, T, outer positions ip[o * cap + s]; returns S or -1 */
+int64_t oracle_dcsr_rows_intersect(int32_t k, const or_matrix *ops, int64_t *rows, int64_t *T, int64_t *ip,
+                                   int64_t cap);
+/* line 4: T' (S + 1 entries) */
+void    oracle_exclusive_prefix(const int64_t *T, int64_t S, int64_t *Tp);
+/* lines 5-6: the remapped partition (row_pos = surviving-row index) */
+int     oracle_partition_remapped(int32_t k, const or_matrix *ops, int64_t S, const int64_t *rows, const int64_t *ip,
+                                  int64_t cap, const int64_t *Tp, int32_t P, or_parts *out);
+/* lines 7-9: Z over the surviving rows (z_pos[S + 1]); returns nnz_Z or -1 */
+int64_t oracle_dcsr_hadamard(int32_t k, const or_matrix *ops, int64_t S, const int64_t *ip, int64_t cap,
+                             int64_t *z_pos, int32_t *z_crd, void *z_val, int64_t zcap);
+
 #ifdef __cplusplus
 }
 #endif
