@@ -206,6 +206,26 @@ nacho_status nacho_inner_k(const nacho_matrix* ops, int32_t k, const nacho_parts
                            size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------------------------
+ * nacho_dcsr_hadamard -- recursive partitioning (Alg. 2) of the DCSR
+ * Hadamard product Z = ops[0] (.) ... (.) ops[k-1] (Listing emul-dcsr2-cfir), whose outer
+ * sparse intersection skips whole rows.  The flow of P:1815-1825 / Listing emul-dcsr2-rewritten
+ * (P:1478-1496): (1) Alg. 1 partitions the outer intersection (the outer levels as one-row operands);
+ * (2) its assembly / prefix sum / compute give the surviving rows rows(A_0) cap ... and
+ * T[i] = C_j(N_j | i), the row's non-zeros over the operands; (3) T' = exclusive prefix sum of T, the
+ * remapped cost C'_i; (4) Alg. 1 with C'_i and the inner nnz cost partitions the
+ * remapped loop nest into `parts` (caller-allocated, parts->P partitions: row_pos = index of the
+ * surviving row, row = its coordinate, pos[o] = absolute positions in crd_o); (5) assembly / prefix
+ * sum / compute of Listing 8's loop body over those partitions.  Output Z in DCSR over the surviving
+ * rows, every one stored even when its column intersection is empty (reading R21): counts[0] = S
+ * (device int64[2]; counts[1] = nnz_Z), z_outer[S] (capacity >= min_o nouter_o), z_pos[S + 1],
+ * z_crd / z_val (capacity >= min_o nnz_o), values the product in operand order (R17).  DCSR operands,
+ * k <= 4; one thread per partition in the assembly / compute kernels (Listing 8's shape). */
+size_t nacho_dcsr_hadamard_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P);
+nacho_status nacho_dcsr_hadamard(const nacho_matrix* ops, int32_t k, nacho_parts* parts, int64_t* counts,
+                                 int32_t* z_outer, int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws,
+                                 size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
  * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.
  * Synchronous on `stream` (it reads one flag back).  Returns NACHO_ERR_FORMAT on a violation. */
 nacho_status nacho_validate(const nacho_matrix* A, void* stream);

@@ -17,6 +17,7 @@
 #include "spadd6.cuh"
 #include "spadd7.cuh"
 #include "dist.cuh"
+#include "recursive.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
 #include "spmv3.cuh"
@@ -649,6 +650,118 @@ nacho_status nacho_inner_k(const nacho_matrix* ops, int32_t k, const nacho_parts
   NACHO_TRY(r);
   s7_sum_partials_kernel<<<1, 1024, 0, st>>>(partial, parts->P, result);
   return launched("s7_sum_partials_kernel");
+}
+
+/* ------------------------------------------------------------------ recursive partitioning (Alg. 2) */
+namespace {
+struct RecLayout {
+  int64_t P1, cap;
+  size_t pos_views, parts1, cnt1, off1, T, ip, Tp, cnt2, off2, total;
+};
+
+RecLayout rec_layout(const nacho_matrix* ops, int32_t k, int32_t P) {
+  RecLayout L;
+  int64_t nouter = 0, cap = INT64_MAX;
+  for (int o = 0; o < k; ++o) { nouter += ops[o].nouter; cap = std::min<int64_t>(cap, ops[o].nouter); }
+  L.cap = cap > 0 ? cap : 1;
+  L.P1 = std::max<int64_t>(1, (nouter + 255) / 256);   // 256 outer entries per partition (one thread each)
+  size_t o = 0;
+  L.pos_views = o; o += align_up((size_t)2 * k * 8);
+  L.parts1 = o; o += parts_bytes(L.P1, k);
+  L.cnt1 = o; o += align_up((size_t)(L.P1 + 1) * 8);
+  L.off1 = o; o += align_up((size_t)(L.P1 + 2) * 8);
+  L.T = o; o += align_up((size_t)L.cap * 8);
+  L.ip = o; o += align_up((size_t)k * L.cap * 8);
+  L.Tp = o; o += align_up((size_t)(L.cap + 2) * 8);
+  L.cnt2 = o; o += align_up((size_t)(P + 1) * 8);
+  L.off2 = o; o += align_up((size_t)(P + 2) * 8);
+  L.total = o;
+  return L;
+}
+}  // namespace
+
+size_t nacho_dcsr_hadamard_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {
+  if (!ops || k < 1 || k > NACHO_MAX_K) return 0;
+  return rec_layout(ops, k, P > 0 ? P : 1).total;
+}
+
+nacho_status nacho_dcsr_hadamard(const nacho_matrix* ops, int32_t k, nacho_parts* parts, int64_t* counts,
+                                 int32_t* z_outer, int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  if (!ops || k < 1 || k > 4) return fail(NACHO_ERR_INVALID_ARG, "k = %d outside [1, 4]", k);
+  for (int o = 0; o < k; ++o) {
+    NACHO_TRY(check_matrix(ops + o, "operand"));
+    if (ops[o].format != NACHO_DCSR) return fail(NACHO_ERR_INVALID_ARG, "recursive partitioning takes DCSR operands");
+    if (ops[o].nrows != ops[0].nrows || ops[o].ncols != ops[0].ncols || ops[o].dtype != ops[0].dtype)
+      return fail(NACHO_ERR_SHAPE, "operand %d disagrees with operand 0", o);
+  }
+  NACHO_TRY(check_parts(parts, k));
+  if (!counts || !z_outer || !z_pos) return fail(NACHO_ERR_INVALID_ARG, "null output");
+  const RecLayout L = rec_layout(ops, k, parts->P);
+  if (!ws || ws_bytes < L.total) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, L.total);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  int64_t* pos_views = reinterpret_cast<int64_t*>(w + L.pos_views);
+  int64_t* cnt1 = reinterpret_cast<int64_t*>(w + L.cnt1);
+  int64_t* off1 = reinterpret_cast<int64_t*>(w + L.off1);
+  int64_t* T = reinterpret_cast<int64_t*>(w + L.T);
+  int64_t* ip = reinterpret_cast<int64_t*>(w + L.ip);
+  int64_t* Tp = reinterpret_cast<int64_t*>(w + L.Tp);
+  int64_t* cnt2 = reinterpret_cast<int64_t*>(w + L.cnt2);
+  int64_t* off2 = reinterpret_cast<int64_t*>(w + L.off2);
+  const int64_t* S_dev = off1 + L.P1;   // the scan's total
+  const OpsArg in = make_ops(ops, k);
+  // 1. the outer intersection partitioned: Alg. 1 over the outer levels as one-row operands
+  rec_outer_views_kernel<<<1, 32, 0, st>>>(in, pos_views);
+  NACHO_TRY(launched("rec_outer_views_kernel"));
+  nacho_matrix views[4];
+  for (int o = 0; o < k; ++o) {
+    views[o] = ops[o];
+    views[o].format = NACHO_CSR;
+    views[o].nrows = 1;
+    views[o].ncols = ops[o].nrows;
+    views[o].nouter = 1;
+    views[o].nnz = ops[o].nouter;
+    views[o].outer_crd = nullptr;
+    views[o].pos = pos_views + 2 * o;
+    views[o].crd = ops[o].outer_crd;
+  }
+  PartsArg p1 = carve_parts(w + L.parts1, L.P1, k);
+  NACHO_TRY(launch_partition(views, k, p1, st));
+  // 2. surviving rows: count, prefix sum (-> S), fill rows / T / outer positions
+  const unsigned g1 = (unsigned)((L.P1 + kRecThreads - 1) / kRecThreads);
+  rec_rows_kernel<0><<<g1, kRecThreads, 0, st>>>(in, p1, cnt1, nullptr, nullptr, nullptr, nullptr, L.cap);
+  NACHO_TRY(launched("rec_rows_kernel<0>"));
+  rec_scan_kernel<1024><<<1, 1024, 0, st>>>(cnt1, nullptr, L.P1, off1);
+  NACHO_TRY(launched("rec_scan_kernel"));
+  rec_rows_kernel<1><<<g1, kRecThreads, 0, st>>>(in, p1, nullptr, off1, z_outer, T, ip, L.cap);
+  NACHO_TRY(launched("rec_rows_kernel<1>"));
+  // 3. T' = exclusive prefix sum of T
+  rec_scan_kernel<1024><<<1, 1024, 0, st>>>(T, S_dev, 0, Tp);
+  NACHO_TRY(launched("rec_scan_kernel"));
+  // 4. the remapped partition
+  const PartsArg p2 = parts_arg(parts);
+  if (k == 1) rec_partition_kernel<1><<<(unsigned)((p2.P + 4) / 4), 128, 0, st>>>(in, p2, S_dev, z_outer, Tp, ip, L.cap);
+  else if (k == 2) rec_partition_kernel<2><<<(unsigned)((p2.P + 4) / 4), 128, 0, st>>>(in, p2, S_dev, z_outer, Tp, ip, L.cap);
+  else rec_partition_kernel<4><<<(unsigned)((p2.P + 4) / 4), 128, 0, st>>>(in, p2, S_dev, z_outer, Tp, ip, L.cap);
+  NACHO_TRY(launched("rec_partition_kernel"));
+  // 5. Z: count, prefix sum, fill (Listing 8 over the remapped rows)
+  const unsigned g2 = (unsigned)((p2.P + kRecThreads - 1) / kRecThreads);
+  const bool f64 = ops[0].dtype == NACHO_F64;
+  if (f64) rec_hadamard_kernel<double, 0><<<g2, kRecThreads, 0, st>>>(in, p2, S_dev, ip, L.cap, cnt2, nullptr, nullptr, nullptr, nullptr);
+  else rec_hadamard_kernel<float, 0><<<g2, kRecThreads, 0, st>>>(in, p2, S_dev, ip, L.cap, cnt2, nullptr, nullptr, nullptr, nullptr);
+  NACHO_TRY(launched("rec_hadamard_kernel<0>"));
+  rec_scan_kernel<1024><<<1, 1024, 0, st>>>(cnt2, nullptr, p2.P, off2);
+  NACHO_TRY(launched("rec_scan_kernel"));
+  if (f64)
+    rec_hadamard_kernel<double, 1><<<g2, kRecThreads, 0, st>>>(in, p2, S_dev, ip, L.cap, nullptr, off2, z_pos, z_crd,
+                                                               static_cast<double*>(z_val));
+  else
+    rec_hadamard_kernel<float, 1><<<g2, kRecThreads, 0, st>>>(in, p2, S_dev, ip, L.cap, nullptr, off2, z_pos, z_crd,
+                                                              static_cast<float*>(z_val));
+  NACHO_TRY(launched("rec_hadamard_kernel<1>"));
+  rec_counts_kernel<<<1, 32, 0, st>>>(S_dev, off2 + p2.P, counts);
+  return launched("rec_counts_kernel");
 }
 
 /* ------------------------------------------------------------------ multi-GPU (dist.cuh) */
