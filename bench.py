@@ -614,6 +614,37 @@ def bench_intersection(N, W, torch, scale, K, Wu, timer):
                               "partition": (P + 1) * (8 * k + 28)}, P=P, dtype="f32", wl=wl, nnz_z=nnz_z)
 
 
+def bench_recursive(N, W, torch, scale, K, Wu, timer):
+    """Recursive partitioning (Alg. 2) on C3-shaped DCSR operands: A = C3, B = the rows of A kept with
+    probability 1/2 (doubled values); one step = nacho_dcsr_hadamard (outer partition, surviving rows,
+    T' prefix sum, remapped partition, assembly, compute).  Thread-per-partition kernels (Listing 8's
+    shape): a coverage line, not a tuned one."""
+    wl = W.build("c3", scale, device="cuda")
+    A = wl.ops[0]
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    keep = torch.rand(A.nouter, device="cuda", generator=g) < 0.5
+    lens = A.pos[1:] - A.pos[:-1]
+    sel = torch.repeat_interleave(keep, lens)
+    bpos = torch.zeros(int(keep.sum().item()) + 1, dtype=torch.int64, device="cuda")
+    torch.cumsum(lens[keep], 0, out=bpos[1:])
+    B = W.SparseMatrix("dcsr", A.nrows, A.ncols, bpos, A.crd[sel].contiguous(), (A.val[sel] * 2).contiguous(),
+                       A.outer_crd[keep].contiguous())
+    ops = [A, B]
+    P = max(1, -(-(A.nnz + B.nnz) // 512))
+
+    def step(timed=False):
+        m = [ev(torch)] if timed else None
+        N.dcsr_hadamard(ops, P)
+        if timed:
+            m.append(ev(torch))
+        return m
+    times, sec = timer.run(step, K, Wu, ["dcsr_hadamard"])
+    read = (A.nnz + B.nnz) * 8 + (A.nouter + B.nouter) * 12
+    return dict(work=A.nnz + B.nnz, times=times, sec=sec, algo_step=read, kernel_bytes={"dcsr_hadamard": read}, P=P,
+                dtype="f32", wl=wl)
+
+
 def bench_spmm(N, W, torch, scale, K, Wu, timer):
     wl = W.build("c4", scale, device="cuda")
     A = wl.ops[0]
@@ -883,6 +914,7 @@ def main():
                          ("c3_spmv_dcsr_f32", lambda: bench_spmv(N, W, torch, "c3", args.scale, 10, 3, timer)),
                          ("c4_spmm_f32_nb64", lambda: bench_spmm(N, W, torch, args.scale, 5, 2, timer)),
                          ("c2_hadamard3_and_inner", lambda: bench_intersection(N, W, torch, args.scale, 10, 3, timer)),
+                         ("c3_dcsr_hadamard_recursive", lambda: bench_recursive(N, W, torch, args.scale, 5, 2, timer)),
                          ("c1_spmv_csr_f64_P8", lambda: bench_spmv(N, W, torch, "c1", 1.0, 20, 3, timer))]:
             try:
                 rr = fn()

@@ -60,6 +60,7 @@ constexpr int kS4Vt = NACHO_S4_VT;                // merged entries per thread a
 constexpr int kS4Tile = kS4Threads * kS4Vt;       // entries per partition
 constexpr int kS4Buf = kS4Tile + kS4Tile / 16 + 8;   // padded stage-buffer capacity (elements)
 constexpr int kS4BlkShift = 8;                    // kS4Stage: partitions per block sum = 256
+static_assert(kS4Threads >= (1 << kS4BlkShift), "s4_place_kernel sums a block's predecessors with one load per thread");
 constexpr int kS4DenseWords = 2048;               // widest column range of the bitmap path (x 32 columns)
 constexpr int kS4PosRound = 8;                    // row pointers loaded per thread and round
 
