@@ -69,6 +69,9 @@ def lib():
         L.oracle_partition_remapped.argtypes = [ctypes.c_int32, vp, i64, vp, vp, i64, vp, ctypes.c_int32, vp]
         L.oracle_dcsr_hadamard.argtypes = [ctypes.c_int32, vp, i64, vp, i64, vp, vp, vp, i64]
         L.oracle_dcsr_hadamard.restype = i64
+        L.oracle_dcsr_spadd_k.argtypes = [ctypes.c_int32, vp, vp, vp, vp, vp, vp, i64, i64]
+        L.oracle_dcsr_spadd_k.restype = i64
+        L.oracle_dcsr_spadd_counts.argtypes = [ctypes.c_int32, vp, vp, vp, vp]
     return _lib
 
 
@@ -285,4 +288,32 @@ def dcsr_hadamard(ops, rm: Remap):
     if n < 0:
         raise ValueError("oracle_dcsr_hadamard failed")
     return rm.rows.astype(np.int32), z_pos, z_crd[:n].copy(), z_val[:n].copy()
+
+
+def dcsr_spadd_k(ops):
+    """(z_outer, z_pos, z_crd, z_val) of the DCSR k-way union (Listing 2)."""
+    arr, keep = _matrices(ops)
+    rcap = max(1, sum(int(A.nouter) for A in ops))
+    zcap = max(1, sum(int(A.crd.shape[0]) for A in ops))
+    z_outer = np.zeros(rcap, np.int32)
+    z_pos = np.zeros(rcap + 1, np.int64)
+    z_crd = np.zeros(zcap, np.int32)
+    z_val = np.zeros(zcap, dtype=ops[0].val.dtype)
+    nr = ctypes.c_int64(0)
+    n = lib().oracle_dcsr_spadd_k(len(ops), arr, _p(z_outer), _p(z_pos), _p(z_crd), _p(z_val), ctypes.byref(nr),
+                                  rcap, zcap)
+    if n < 0:
+        raise ValueError("oracle_dcsr_spadd_k failed (DCSR operands only)")
+    r = nr.value
+    return z_outer[:r].copy(), z_pos[:r + 1].copy(), z_crd[:n].copy(), z_val[:n].copy()
+
+
+def dcsr_spadd_counts(ops, parts: Parts):
+    arr, keep = _matrices(ops)
+    ent = np.zeros(parts.P, np.int64)
+    rows = np.zeros(parts.P, np.int64)
+    s = parts.c()
+    if lib().oracle_dcsr_spadd_counts(len(ops), arr, ctypes.byref(s), _p(ent), _p(rows)) != 0:
+        raise ValueError("oracle_dcsr_spadd_counts failed")
+    return ent, rows
 

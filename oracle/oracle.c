@@ -605,3 +605,95 @@ int64_t oracle_dcsr_hadamard(int32_t k, const or_matrix *ops, int64_t S, const i
     return nz;
 }
 
+/* ---------------------------------------------------------- DCSR k-way SpAdd */
+/*
+ * Z = A_0 + ... + A_{k-1} on DCSR operands: Listing 2 (lst:eadd-dcsr2-cfir) literally --
+ *   while i <- rows(A_0) cup ... :  while j <- cols(A_0[i]) cup ... :  Z[i, j] = sum_o A_o[i, j]
+ * with the k-finger merges of Listing 1 in union form at both levels; values the left fold in operand
+ * order from the first present value (R9).  Z is DCSR: its outer level is the union of the operands'
+ * stored rows, all non-empty (R10).  Capacities: z_outer >= sum nouter, z_pos >= that + 1, z_crd /
+ * z_val >= sum nnz.  Returns nnz_Z (z_nrows receives the number of stored rows), or -1.
+ */
+int64_t oracle_dcsr_spadd_k(int32_t k, const or_matrix *ops, int32_t *z_outer, int64_t *z_pos, int32_t *z_crd,
+                            void *z_val, int64_t *z_nrows, int64_t rcap, int64_t zcap) {
+    for (int32_t o = 0; o < k; o++) if (ops[o].format != OR_DCSR) return -1;
+    const int f64 = ops[0].dtype == OR_F64;
+    int64_t *qi = (int64_t *)calloc((size_t)k, sizeof(int64_t));   /* outer cursors */
+    int64_t *q = (int64_t *)calloc((size_t)k, sizeof(int64_t));    /* inner cursors */
+    int64_t *e = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t nz = 0, nr = 0;
+    z_pos[0] = 0;
+    for (;;) {
+        int64_t r = -1;
+        for (int32_t o = 0; o < k; o++)
+            if (qi[o] < ops[o].nouter && (r < 0 || ops[o].outer_crd[qi[o]] < r)) r = ops[o].outer_crd[qi[o]];
+        if (r < 0) break;
+        for (int32_t o = 0; o < k; o++) {
+            if (qi[o] < ops[o].nouter && ops[o].outer_crd[qi[o]] == r) { q[o] = ops[o].pos[qi[o]]; e[o] = ops[o].pos[qi[o] + 1]; }
+            else { q[o] = 0; e[o] = 0; }
+        }
+        for (;;) {
+            int64_t j = -1;
+            for (int32_t o = 0; o < k; o++) if (q[o] < e[o] && (j < 0 || ops[o].crd[q[o]] < j)) j = ops[o].crd[q[o]];
+            if (j < 0) break;
+            double vd = 0.0; float vf = 0.0f; int have = 0;
+            for (int32_t o = 0; o < k; o++) {
+                if (q[o] < e[o] && ops[o].crd[q[o]] == j) {
+                    if (f64) { double a = ((const double *)ops[o].val)[q[o]]; vd = have ? vd + a : a; }
+                    else     { float  a = ((const float *)ops[o].val)[q[o]];  vf = have ? vf + a : a; }
+                    have = 1;
+                    q[o]++;
+                }
+            }
+            if (nz >= zcap) { free(qi); free(q); free(e); return -1; }
+            z_crd[nz] = (int32_t)j;
+            if (f64) ((double *)z_val)[nz] = vd; else ((float *)z_val)[nz] = vf;
+            nz++;
+        }
+        if (nr >= rcap) { free(qi); free(q); free(e); return -1; }
+        z_outer[nr] = (int32_t)r;
+        z_pos[nr + 1] = nz;
+        nr++;
+        for (int32_t o = 0; o < k; o++) if (qi[o] < ops[o].nouter && ops[o].outer_crd[qi[o]] == r) qi[o]++;
+    }
+    free(qi); free(q); free(e);
+    *z_nrows = nr;
+    return nz;
+}
+
+/* Per-partition assembly counts of the DCSR union for given boundaries: ent[p] = #union coordinates c
+ * with b_p <=lex c <lex b_{p+1}; rows[p] = #union rows whose first union coordinate lies there (the
+ * partition that appends the row to Z's outer level). */
+int oracle_dcsr_spadd_counts(int32_t k, const or_matrix *ops, const or_parts *parts, int64_t *ent, int64_t *rows) {
+    for (int32_t o = 0; o < k; o++) if (ops[o].format != OR_DCSR) return 1;
+    const int32_t P = parts->P;
+    int64_t *qi = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t *q = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t *e = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    for (int32_t p = 0; p < P; p++) { ent[p] = 0; rows[p] = 0; }
+    int32_t p = 0;
+    for (;;) {
+        int64_t r = -1;
+        for (int32_t o = 0; o < k; o++)
+            if (qi[o] < ops[o].nouter && (r < 0 || ops[o].outer_crd[qi[o]] < r)) r = ops[o].outer_crd[qi[o]];
+        if (r < 0) break;
+        for (int32_t o = 0; o < k; o++) {
+            if (qi[o] < ops[o].nouter && ops[o].outer_crd[qi[o]] == r) { q[o] = ops[o].pos[qi[o]]; e[o] = ops[o].pos[qi[o] + 1]; }
+            else { q[o] = 0; e[o] = 0; }
+        }
+        int first = 1;
+        for (;;) {
+            int64_t j = -1;
+            for (int32_t o = 0; o < k; o++) if (q[o] < e[o] && (j < 0 || ops[o].crd[q[o]] < j)) j = ops[o].crd[q[o]];
+            if (j < 0) break;
+            while (p + 1 < P && (r > parts->row[p + 1] || (r == parts->row[p + 1] && j >= parts->col[p + 1]))) p++;
+            ent[p]++;
+            if (first) { rows[p]++; first = 0; }
+            for (int32_t o = 0; o < k; o++) if (q[o] < e[o] && ops[o].crd[q[o]] == j) q[o]++;
+        }
+        for (int32_t o = 0; o < k; o++) if (qi[o] < ops[o].nouter && ops[o].outer_crd[qi[o]] == r) qi[o]++;
+    }
+    free(qi); free(q); free(e);
+    return 0;
+}
+

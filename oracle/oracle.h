@@ -93,6 +93,13 @@ int     oracle_partition_remapped(int32_t k, const or_matrix *ops, int64_t S, co
 int64_t oracle_dcsr_hadamard(int32_t k, const or_matrix *ops, int64_t S, const int64_t *ip, int64_t cap,
                              int64_t *z_pos, int32_t *z_crd, void *z_val, int64_t zcap);
 
+/* Z = sum_o ops[o] on DCSR operands (Listing 2): Z DCSR over the union of the stored rows; returns
+ * nnz_Z (z_nrows = stored rows of Z) or -1 */
+int64_t oracle_dcsr_spadd_k(int32_t k, const or_matrix *ops, int32_t *z_outer, int64_t *z_pos, int32_t *z_crd,
+                            void *z_val, int64_t *z_nrows, int64_t rcap, int64_t zcap);
+/* per-partition union entries and rows started, DCSR operands */
+int     oracle_dcsr_spadd_counts(int32_t k, const or_matrix *ops, const or_parts *parts, int64_t *ent, int64_t *rows);
+
 #ifdef __cplusplus
 }
 #endif
