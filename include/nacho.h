@@ -226,6 +226,20 @@ nacho_status nacho_dcsr_hadamard(const nacho_matrix* ops, int32_t k, nacho_parts
                                  size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------------------------
+ * nacho_dcsr_spadd_k -- Z = ops[0] + ... + ops[k-1] on DCSR operands (Listing 2, lst:eadd-dcsr2-cfir,
+ * P:568-574) over the partition `parts` made by nacho_partition on the same DCSR
+ * operands (Alg. 1 with k compressed outer levels: the row cost sum_o pos_o[lb_o(x)], P:1670-1672;
+ * row_pos = the boundary row's lower bound in operand 0's outer level).  Assembly (union entries and
+ * rows started per partition), prefix sums, compute (one thread per partition, Listing 8's shape):
+ * Z is DCSR over the union of the stored rows: counts[0] = its stored rows, counts[1] = nnz_Z (device
+ * int64[2]); z_outer / z_pos capacity >= sum_o nouter_o (+1), z_crd / z_val >= sum_o nnz_o; values fold
+ * left in operand order (R9).  k <= 4. */
+size_t nacho_dcsr_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P);
+nacho_status nacho_dcsr_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* counts,
+                                int32_t* z_outer, int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws,
+                                size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
  * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.
  * Synchronous on `stream` (it reads one flag back).  Returns NACHO_ERR_FORMAT on a violation. */
 nacho_status nacho_validate(const nacho_matrix* A, void* stream);

@@ -77,6 +77,9 @@ def _load():
     L.nacho_dcsr_hadamard_workspace_size.argtypes = [vp, i32, i32]
     L.nacho_dcsr_hadamard_workspace_size.restype = sz
     L.nacho_dcsr_hadamard.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_dcsr_spadd_k_workspace_size.argtypes = [vp, i32, i32]
+    L.nacho_dcsr_spadd_k_workspace_size.restype = sz
+    L.nacho_dcsr_spadd_k.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     # multi-GPU (dist.cuh)
     L.nacho_dist_unique_id_size.restype = sz
     L.nacho_dist_unique_id.argtypes = [vp]
@@ -102,7 +105,8 @@ EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", 
            "nacho_spadd_k_staged_workspace_size", "nacho_spadd_k_staged",
            "nacho_spmm_workspace_size", "nacho_spmm", "nacho_validate", "nacho_last_error",
            "nacho_launch_count", "nacho_hadamard_k", "nacho_inner_k_workspace_size", "nacho_inner_k",
-           "nacho_dcsr_hadamard_workspace_size", "nacho_dcsr_hadamard",
+           "nacho_dcsr_hadamard_workspace_size", "nacho_dcsr_hadamard", "nacho_dcsr_spadd_k_workspace_size",
+           "nacho_dcsr_spadd_k",
            "nacho_dist_unique_id_size", "nacho_dist_unique_id", "nacho_dist_init",
            "nacho_dist_destroy", "nacho_dist_broadcast", "nacho_device_cuts", "nacho_shard_rows", "nacho_dist_seam",
            "nacho_dist_spmv_workspace_size", "nacho_dist_spmv", "nacho_dist_spadd_workspace_size",
@@ -391,6 +395,28 @@ def dcsr_hadamard(ops, P: int = None, stream=None):
                                    _ptr(z_val), _ptr(ws), need, _stream(stream)))
     S, nnz = (int(v) for v in counts.cpu().tolist())
     return parts, z_outer[:S], z_pos[:S + 1], z_crd[:nnz], z_val[:nnz]
+
+
+def dcsr_spadd_k(ops, parts: Parts, stream=None):
+    """nacho_dcsr_spadd_k: Z = sum of DCSR operands over `parts` (nacho_partition on the same operands).
+    Returns (z_outer, z_pos, z_crd, z_val) trimmed to Z's stored rows and nnz_Z (one host read)."""
+    arr = _matrices(ops)
+    dev = ops[0].pos.device
+    k = len(ops)
+    cap_r = max(1, sum(int(A.pos.shape[0]) - 1 for A in ops))
+    cap_z = max(1, sum(int(A.crd.shape[0]) for A in ops))
+    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    z_outer = torch.empty(cap_r, dtype=torch.int32, device=dev)
+    z_pos = torch.zeros(cap_r + 1, dtype=torch.int64, device=dev)
+    z_crd = torch.empty(cap_z, dtype=torch.int32, device=dev)
+    z_val = torch.empty(cap_z, dtype=ops[0].val.dtype, device=dev)
+    need = lib.nacho_dcsr_spadd_k_workspace_size(arr, k, parts.P)
+    ws, _ = _workspace(need, dev)
+    pc = parts.c()
+    _check(lib.nacho_dcsr_spadd_k(arr, k, ctypes.byref(pc), _ptr(counts), _ptr(z_outer), _ptr(z_pos), _ptr(z_crd),
+                                  _ptr(z_val), _ptr(ws), need, _stream(stream)))
+    nr, nnz = (int(v) for v in counts.cpu().tolist())
+    return z_outer[:nr], z_pos[:nr + 1], z_crd[:nnz], z_val[:nnz]
 
 
 # ------------------------------------------------------------------ multi-GPU (include/nacho.h, dist.cuh)

@@ -18,6 +18,7 @@
 #include "spadd7.cuh"
 #include "dist.cuh"
 #include "recursive.cuh"
+#include "dcsr_add.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
 #include "spmv3.cuh"
@@ -114,7 +115,7 @@ nacho_status check_ops(const nacho_matrix* ops, int32_t k) {
         ops[o].dtype != ops[0].dtype)
       return fail(NACHO_ERR_SHAPE, "operand %d disagrees with operand 0 in format/shape/dtype", o);
   }
-  if (ops[0].format == NACHO_DCSR && k > 1) return fail(NACHO_ERR_INVALID_ARG, "DCSR partitioning supports k == 1");
+  if (ops[0].format == NACHO_DCSR && k > 4) return fail(NACHO_ERR_INVALID_ARG, "DCSR partitioning supports k <= 4");
   return NACHO_SUCCESS;
 }
 
@@ -189,6 +190,12 @@ nacho_status launch_partition(const nacho_matrix* ops, int32_t k, const PartsArg
   if (k == 1) {
     partition1_kernel<<<(unsigned)((int64_t(pa.P) + 256) / 256), 256, 0, st>>>(a, pa, q, Ptot, p0);
     return launched("partition1_kernel");
+  }
+  if (ops[0].format == NACHO_DCSR) {   // k compressed outer levels (dcsr_add.cuh)
+    const unsigned g = (unsigned)((int64_t(pa.P) + 4) / 4);
+    if (k == 2) dcsr_partition_kernel<2><<<g, 128, 0, st>>>(a, pa, q);
+    else dcsr_partition_kernel<4><<<g, 128, 0, st>>>(a, pa, q);
+    return launched("dcsr_partition_kernel");
   }
   const int64_t nb = (int64_t(pa.P) + 1 + kPartWarps - 1) / kPartWarps;
   if (k == 2) partition_kernel<kPartWarps, 2><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q, Ptot, p0);
@@ -761,6 +768,52 @@ nacho_status nacho_dcsr_hadamard(const nacho_matrix* ops, int32_t k, nacho_parts
                                                               static_cast<float*>(z_val));
   NACHO_TRY(launched("rec_hadamard_kernel<1>"));
   rec_counts_kernel<<<1, 32, 0, st>>>(S_dev, off2 + p2.P, counts);
+  return launched("rec_counts_kernel");
+}
+
+/* ------------------------------------------------------------------ DCSR k-way SpAdd (Listing 2) */
+size_t nacho_dcsr_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {
+  (void)ops; (void)k;
+  const size_t Pe = P > 0 ? P : 1;
+  return 2 * align_up((Pe + 1) * 8) + 2 * align_up((Pe + 2) * 8);
+}
+
+nacho_status nacho_dcsr_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* counts,
+                                int32_t* z_outer, int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws,
+                                size_t ws_bytes, void* stream) {
+  NACHO_TRY(check_ops(ops, k));
+  if (ops[0].format != NACHO_DCSR) return fail(NACHO_ERR_INVALID_ARG, "nacho_dcsr_spadd_k takes DCSR operands");
+  NACHO_TRY(check_parts(parts, k));
+  if (!counts || !z_outer || !z_pos) return fail(NACHO_ERR_INVALID_ARG, "null output");
+  if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
+  const int64_t P = parts->P;
+  const size_t need = nacho_dcsr_spadd_k_workspace_size(ops, k, parts->P);
+  if (!ws || ws_bytes < need) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  int64_t* ent = reinterpret_cast<int64_t*>(w);
+  int64_t* rst = reinterpret_cast<int64_t*>(w + align_up((P + 1) * 8));
+  int64_t* off_e = reinterpret_cast<int64_t*>(w + 2 * align_up((P + 1) * 8));
+  int64_t* off_r = reinterpret_cast<int64_t*>(w + 2 * align_up((P + 1) * 8) + align_up((P + 2) * 8));
+  const OpsArg a = make_ops(ops, k);
+  const PartsArg pa = parts_arg(parts);
+  const unsigned g = (unsigned)((P + 127) / 128);
+  const bool f64 = ops[0].dtype == NACHO_F64;
+  if (f64) dcsr_spadd_kernel<double, 0><<<g, 128, 0, st>>>(a, pa, ent, rst, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  else dcsr_spadd_kernel<float, 0><<<g, 128, 0, st>>>(a, pa, ent, rst, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  NACHO_TRY(launched("dcsr_spadd_kernel<0>"));
+  rec_scan_kernel<1024><<<1, 1024, 0, st>>>(ent, nullptr, P, off_e);
+  NACHO_TRY(launched("rec_scan_kernel"));
+  rec_scan_kernel<1024><<<1, 1024, 0, st>>>(rst, nullptr, P, off_r);
+  NACHO_TRY(launched("rec_scan_kernel"));
+  if (f64)
+    dcsr_spadd_kernel<double, 1><<<g, 128, 0, st>>>(a, pa, nullptr, nullptr, off_e, off_r, z_outer, z_pos, z_crd,
+                                                     static_cast<double*>(z_val));
+  else
+    dcsr_spadd_kernel<float, 1><<<g, 128, 0, st>>>(a, pa, nullptr, nullptr, off_e, off_r, z_outer, z_pos, z_crd,
+                                                    static_cast<float*>(z_val));
+  NACHO_TRY(launched("dcsr_spadd_kernel<1>"));
+  rec_counts_kernel<<<1, 32, 0, st>>>(off_r + P, off_e + P, counts);
   return launched("rec_counts_kernel");
 }
 
