@@ -72,6 +72,8 @@ def lib():
         L.oracle_dcsr_spadd_k.argtypes = [ctypes.c_int32, vp, vp, vp, vp, vp, vp, i64, i64]
         L.oracle_dcsr_spadd_k.restype = i64
         L.oracle_dcsr_spadd_counts.argtypes = [ctypes.c_int32, vp, vp, vp, vp]
+        L.oracle_mixed_spadd_k.argtypes = [ctypes.c_int32, vp, vp, vp, vp, i64]
+        L.oracle_mixed_spadd_k.restype = i64
     return _lib
 
 
@@ -88,7 +90,7 @@ def _matrices(ops):
         val = np.ascontiguousarray(A.val)
         outer = None if A.outer_crd is None else np.ascontiguousarray(A.outer_crd, dtype=np.int32)
         keep += [pos, crd, val, outer]
-        arr[i].format = 0 if A.format == "csr" else 1
+        arr[i].format = {"csr": 0, "dcsr": 1, "coo": 2}[A.format]
         arr[i].dtype = 1 if val.dtype == np.float64 else 0
         arr[i].nrows, arr[i].ncols = A.nrows, A.ncols
         arr[i].nnz = crd.shape[0]
@@ -316,4 +318,17 @@ def dcsr_spadd_counts(ops, parts: Parts):
     if lib().oracle_dcsr_spadd_counts(len(ops), arr, ctypes.byref(s), _p(ent), _p(rows)) != 0:
         raise ValueError("oracle_dcsr_spadd_counts failed")
     return ent, rows
+
+
+def mixed_spadd_k(ops):
+    """(z_pos, z_crd, z_val): CSR Z of CSR and COO operands mixed (the union per row, left fold)."""
+    arr, keep = _matrices(ops)
+    cap = max(1, sum(int(A.crd.shape[0]) for A in ops))
+    z_pos = np.zeros(ops[0].nrows + 1, np.int64)
+    z_crd = np.zeros(cap, np.int32)
+    z_val = np.zeros(cap, dtype=ops[0].val.dtype)
+    n = lib().oracle_mixed_spadd_k(len(ops), arr, _p(z_pos), _p(z_crd), _p(z_val), cap)
+    if n < 0:
+        raise ValueError("oracle_mixed_spadd_k failed (CSR / COO operands only)")
+    return z_pos, z_crd[:n].copy(), z_val[:n].copy()
 

@@ -19,7 +19,7 @@ static long double vget_ld(const or_matrix *A, int64_t q) {
 }
 /* row coordinate of outer position ip (P:1679 CSR dense row level; P:562 DCSR compressed row level) */
 static int64_t row_of(const or_matrix *A, int64_t ip) {
-    return A->format == OR_DCSR ? (int64_t)A->outer_crd[ip] : ip;
+    return A->format == OR_CSR ? ip : (int64_t)A->outer_crd[ip];   /* COO: ip is the entry */
 }
 
 /* lb_search of Listing 7: "Find least ipA in [lA, hA] s.t. A[ipA] >= i".
@@ -78,13 +78,13 @@ static void set_origin(int32_t k, or_parts *out, int32_t p) {
 }
 static void set_end(int32_t k, const or_matrix *ops, or_parts *out, int32_t p) {
     out->row[p] = ops[0].nrows;
-    out->row_pos[p] = ops[0].nouter;
+    out->row_pos[p] = ops[0].format == OR_DCSR ? ops[0].nouter : ops[0].nrows;   /* COO: the dense row index */
     out->col[p] = 0;
     for (int32_t o = 0; o < k; o++) out->pos[(int64_t)p * k + o] = ops[o].nnz;
 }
 /* number of stored rows of operand 0 with coordinate < row (CSR: row itself) */
 static int64_t outer_lb(const or_matrix *A, int64_t row) {
-    if (A->format == OR_CSR) return row;
+    if (A->format != OR_DCSR) return row;   /* CSR and COO: the dense row index */
     int64_t a = 0, b = A->nouter;
     while (a < b) { int64_t m = a + (b - a) / 2; if ((int64_t)A->outer_crd[m] >= row) b = m; else a = m + 1; }
     return a;
@@ -112,7 +112,8 @@ int oracle_partition_rank(int32_t k, const or_matrix *ops, int32_t P, or_parts *
         int64_t best_r = -1, best_c = -1;
         for (int32_t o = 0; o < k; o++) {
             if (q[o] >= ops[o].nnz) continue;
-            while (ops[o].pos[ip[o] + 1] <= q[o]) ip[o]++;           /* outer position holding q[o] */
+            if (ops[o].format == OR_COO) ip[o] = q[o];                  /* COO: the row level is per entry */
+            else while (ops[o].pos[ip[o] + 1] <= q[o]) ip[o]++;      /* outer position holding q[o] */
             int64_t r = row_of(&ops[o], ip[o]), cc = ops[o].crd[q[o]];
             if (best_r < 0 || r < best_r || (r == best_r && cc < best_c)) { best_r = r; best_c = cc; }
         }
@@ -695,5 +696,51 @@ int oracle_dcsr_spadd_counts(int32_t k, const or_matrix *ops, const or_parts *pa
     }
     free(qi); free(q); free(e);
     return 0;
+}
+
+/* ------------------------------------------------------ mixed CSR / COO k-way SpAdd */
+/* The row segment of operand o: CSR [pos[i], pos[i+1]); COO the entries whose row is i (a cursor that
+ * moves forward over the sorted row level). */
+int64_t oracle_mixed_spadd_k(int32_t k, const or_matrix *ops, int64_t *z_pos, int32_t *z_crd, void *z_val,
+                             int64_t capacity) {
+    for (int32_t o = 0; o < k; o++) if (ops[o].format == OR_DCSR) return -1;
+    const int64_t M = ops[0].nrows;
+    const int f64 = ops[0].dtype == OR_F64;
+    int64_t *q = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t *e = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t *cc = (int64_t *)calloc((size_t)k, sizeof(int64_t));   /* COO cursors */
+    int64_t nz = 0;
+    z_pos[0] = 0;
+    for (int64_t i = 0; i < M; i++) {
+        for (int32_t o = 0; o < k; o++) {
+            if (ops[o].format == OR_CSR) { q[o] = ops[o].pos[i]; e[o] = ops[o].pos[i + 1]; }
+            else {
+                q[o] = cc[o];
+                while (cc[o] < ops[o].nnz && ops[o].outer_crd[cc[o]] == i) cc[o]++;
+                e[o] = cc[o];
+            }
+        }
+        for (;;) {
+            int64_t j = -1;
+            for (int32_t o = 0; o < k; o++) if (q[o] < e[o] && (j < 0 || ops[o].crd[q[o]] < j)) j = ops[o].crd[q[o]];
+            if (j < 0) break;
+            double vd = 0.0; float vf = 0.0f; int have = 0;
+            for (int32_t o = 0; o < k; o++) {
+                if (q[o] < e[o] && ops[o].crd[q[o]] == j) {
+                    if (f64) { double a = ((const double *)ops[o].val)[q[o]]; vd = have ? vd + a : a; }
+                    else     { float  a = ((const float *)ops[o].val)[q[o]];  vf = have ? vf + a : a; }
+                    have = 1;
+                    q[o]++;
+                }
+            }
+            if (nz >= capacity) { free(q); free(e); free(cc); return -1; }
+            z_crd[nz] = (int32_t)j;
+            if (f64) ((double *)z_val)[nz] = vd; else ((float *)z_val)[nz] = vf;
+            nz++;
+        }
+        z_pos[i + 1] = nz;
+    }
+    free(q); free(e); free(cc);
+    return nz;
 }
 

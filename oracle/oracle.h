@@ -24,6 +24,7 @@ extern "C" {
 
 #define OR_CSR  0
 #define OR_DCSR 1
+#define OR_COO  2   /* Compressed(non-unique) o Singleton: pos = [0, nnz], outer_crd = row of every entry */
 #define OR_F32  0
 #define OR_F64  1
 
@@ -99,6 +100,11 @@ int64_t oracle_dcsr_spadd_k(int32_t k, const or_matrix *ops, int32_t *z_outer, i
                             void *z_val, int64_t *z_nrows, int64_t rcap, int64_t zcap);
 /* per-partition union entries and rows started, DCSR operands */
 int     oracle_dcsr_spadd_counts(int32_t k, const or_matrix *ops, const or_parts *parts, int64_t *ent, int64_t *rows);
+
+/* Z = sum_o ops[o] for CSR and COO operands mixed (the COO + CSR addition of P:2449-2470): the
+ * union per row, left fold; Z is CSR (z_pos[nrows + 1]).  Returns nnz_Z or -1. */
+int64_t oracle_mixed_spadd_k(int32_t k, const or_matrix *ops, int64_t *z_pos, int32_t *z_crd, void *z_val,
+                             int64_t capacity);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,7 @@ from . import recipe as R
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
-CSR, DCSR = "csr", "dcsr"
+CSR, DCSR, COO = "csr", "dcsr", "coo"
 
 
 @dataclass
@@ -28,7 +28,7 @@ class SparseMatrix:
     pos: object            # int64 [nouter+1]
     crd: object            # int32 [nnz]
     val: object            # float32/float64 [nnz]
-    outer_crd: object = None   # int32 [nouter] (DCSR)
+    outer_crd: object = None   # int32 [nouter] (DCSR); COO: the row of every entry [nnz], pos = [0, nnz]
 
     @property
     def nnz(self) -> int:
@@ -90,6 +90,10 @@ def from_coo(rows, cols, vals, nrows, ncols, fmt=CSR, dtype=np.float32) -> Spars
 def to_dense(A: SparseMatrix) -> np.ndarray:
     A = A.numpy()
     D = np.zeros((A.nrows, A.ncols), dtype=np.float64)
+    if A.format == COO:
+        for q in range(A.nnz):
+            D[int(A.outer_crd[q]), int(A.crd[q])] = A.val[q]
+        return D
     for ip in range(A.nouter):
         r = ip if A.format == CSR else int(A.outer_crd[ip])
         for q in range(int(A.pos[ip]), int(A.pos[ip + 1])):
@@ -342,3 +346,20 @@ def dense_x(name: str, scale: float = 1.0, device: str = "cuda"):
     cfg = scaled(CONFIGS[name], scale)
     gen = _DeviceGen(cfg, "uniform", 4, device)
     return gen.dense(R.S_X, cfg["m"], 1)
+
+
+def to_coo(A: SparseMatrix) -> SparseMatrix:
+    """The COO form of a CSR operand (TACO's Compressed(non-unique) o Singleton: pos = [0, nnz], the
+    row level one coordinate per entry).  Test fixtures and setup only."""
+    if A.format != CSR:
+        raise ValueError("to_coo takes a CSR operand")
+    if isinstance(A.pos, np.ndarray):
+        rows = np.repeat(np.arange(A.nrows, dtype=np.int32), np.diff(A.pos))
+        pos = np.array([0, A.nnz], np.int64)
+    else:
+        import torch
+        rows = torch.repeat_interleave(torch.arange(A.nrows, dtype=torch.int32, device=A.pos.device),
+                                       A.pos[1:] - A.pos[:-1])
+        pos = torch.tensor([0, A.nnz], dtype=torch.int64, device=A.pos.device)
+    return SparseMatrix(COO, A.nrows, A.ncols, pos, A.crd, A.val, rows)
+
