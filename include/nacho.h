@@ -37,7 +37,7 @@ typedef enum {
   NACHO_ERR_NCCL = 7         /* NCCL not loadable, or an NCCL call failed (multi-GPU calls only) */
 } nacho_status;
 
-typedef enum { NACHO_CSR = 0, NACHO_DCSR = 1 } nacho_format;
+typedef enum { NACHO_CSR = 0, NACHO_DCSR = 1, NACHO_COO = 2 } nacho_format;
 typedef enum { NACHO_F32 = 0, NACHO_F64 = 1 } nacho_dtype;
 
 #define NACHO_MAX_K 8
@@ -46,7 +46,10 @@ typedef enum { NACHO_F32 = 0, NACHO_F64 = 1 } nacho_dtype;
  *   CSR  = Dense(rows) o Compressed(cols)       -- pos[nrows+1], crd[nnz]
  *   DCSR = Compressed(rows) o Compressed(cols)  -- outer_crd[nouter], pos[nouter+1]
  * pos[0] = 0, pos non-decreasing, pos[nouter] = nnz; crd strictly increasing within each row
- * segment and < ncols; DCSR outer_crd strictly increasing and every stored row non-empty (R10). */
+ * segment and < ncols; DCSR outer_crd strictly increasing and every stored row non-empty (R10).
+ *   COO  = Compressed(non-unique)(rows) o Singleton(cols): nouter = 1, pos = [0, nnz],
+ *          outer_crd[nnz] = the row of every entry (sorted by (row, col), no duplicates).  COO operands
+ *          are taken by nacho_partition and nacho_mixed_spadd_k (mixed with CSR operands) only. */
 typedef struct {
   int32_t format;            /* nacho_format */
   int32_t dtype;             /* nacho_dtype of val */
@@ -238,6 +241,17 @@ size_t nacho_dcsr_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int
 nacho_status nacho_dcsr_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* counts,
                                 int32_t* z_outer, int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws,
                                 size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * nacho_mixed_spadd_k -- Z = ops[0] + ... + ops[k-1] for CSR and COO operands mixed (the COO + CSR
+ * addition the paper evaluates without a format conversion) over the
+ * partition nacho_partition made of the same operands (Alg. 1 with the COO row level: C_i(x) counts
+ * the entries whose row is < x, a binary search per probe).  One thread per partition (Listing 8's
+ * shape): count, prefix sum, fill.  Z is CSR: z_pos[nrows + 1], z_crd / z_val capacity >= sum_o nnz_o,
+ * nnz_z (device int64[1]).  Values fold left in operand order (R9).  k <= 4. */
+size_t nacho_mixed_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P);
+nacho_status nacho_mixed_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* nnz_z,
+                                 int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------------------------
  * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.

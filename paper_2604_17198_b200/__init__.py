@@ -17,7 +17,7 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NACHO_LIB", os.path.join(HERE, "libnacho.so"))
 
-NACHO_CSR, NACHO_DCSR = 0, 1
+NACHO_CSR, NACHO_DCSR, NACHO_COO = 0, 1, 2
 NACHO_F32, NACHO_F64 = 0, 1
 MAX_K = 8
 STATUS = {0: "SUCCESS", 1: "INVALID_ARG", 2: "SHAPE", 3: "FORMAT", 4: "OVERFLOW", 5: "WORKSPACE", 6: "CUDA",
@@ -80,6 +80,9 @@ def _load():
     L.nacho_dcsr_spadd_k_workspace_size.argtypes = [vp, i32, i32]
     L.nacho_dcsr_spadd_k_workspace_size.restype = sz
     L.nacho_dcsr_spadd_k.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_mixed_spadd_k_workspace_size.argtypes = [vp, i32, i32]
+    L.nacho_mixed_spadd_k_workspace_size.restype = sz
+    L.nacho_mixed_spadd_k.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]
     # multi-GPU (dist.cuh)
     L.nacho_dist_unique_id_size.restype = sz
     L.nacho_dist_unique_id.argtypes = [vp]
@@ -106,7 +109,7 @@ EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", 
            "nacho_spmm_workspace_size", "nacho_spmm", "nacho_validate", "nacho_last_error",
            "nacho_launch_count", "nacho_hadamard_k", "nacho_inner_k_workspace_size", "nacho_inner_k",
            "nacho_dcsr_hadamard_workspace_size", "nacho_dcsr_hadamard", "nacho_dcsr_spadd_k_workspace_size",
-           "nacho_dcsr_spadd_k",
+           "nacho_dcsr_spadd_k", "nacho_mixed_spadd_k_workspace_size", "nacho_mixed_spadd_k",
            "nacho_dist_unique_id_size", "nacho_dist_unique_id", "nacho_dist_init",
            "nacho_dist_destroy", "nacho_dist_broadcast", "nacho_device_cuts", "nacho_shard_rows", "nacho_dist_seam",
            "nacho_dist_spmv_workspace_size", "nacho_dist_spmv", "nacho_dist_spadd_workspace_size",
@@ -144,7 +147,7 @@ def matrix(A) -> Matrix:
         raise TypeError("val must be float32 or float64")
     _require(A.val, A.val.dtype, "val")
     m = Matrix()
-    m.format = NACHO_CSR if A.format == "csr" else NACHO_DCSR
+    m.format = {"csr": NACHO_CSR, "dcsr": NACHO_DCSR, "coo": NACHO_COO}[A.format]
     m.dtype = NACHO_F64 if A.val.dtype == torch.float64 else NACHO_F32
     m.nrows, m.ncols = int(A.nrows), int(A.ncols)
     m.nnz = int(A.crd.shape[0])
@@ -417,6 +420,26 @@ def dcsr_spadd_k(ops, parts: Parts, stream=None):
                                   _ptr(z_val), _ptr(ws), need, _stream(stream)))
     nr, nnz = (int(v) for v in counts.cpu().tolist())
     return z_outer[:nr], z_pos[:nr + 1], z_crd[:nnz], z_val[:nnz]
+
+
+def mixed_spadd_k(ops, parts: Parts, stream=None):
+    """nacho_mixed_spadd_k: Z (CSR) = sum of CSR / COO operands over `parts`.  Returns (z_pos, z_crd,
+    z_val) trimmed to nnz_Z (one host read)."""
+    arr = _matrices(ops)
+    dev = ops[0].pos.device
+    k = len(ops)
+    cap = max(1, sum(int(A.crd.shape[0]) for A in ops))
+    nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+    z_pos = torch.empty(ops[0].nrows + 1, dtype=torch.int64, device=dev)
+    z_crd = torch.empty(cap, dtype=torch.int32, device=dev)
+    z_val = torch.empty(cap, dtype=ops[0].val.dtype, device=dev)
+    need = lib.nacho_mixed_spadd_k_workspace_size(arr, k, parts.P)
+    ws, _ = _workspace(need, dev)
+    pc = parts.c()
+    _check(lib.nacho_mixed_spadd_k(arr, k, ctypes.byref(pc), _ptr(nnz), _ptr(z_pos), _ptr(z_crd), _ptr(z_val),
+                                   _ptr(ws), need, _stream(stream)))
+    n = int(nnz.item())
+    return z_pos, z_crd[:n], z_val[:n]
 
 
 # ------------------------------------------------------------------ multi-GPU (include/nacho.h, dist.cuh)

@@ -93,7 +93,10 @@ int64_t spmv_tile(int dtype) {   // positions per tile of the SpMV kernel in use
 
 nacho_status check_matrix(const nacho_matrix* A, const char* name) {
   if (!A) return fail(NACHO_ERR_INVALID_ARG, "%s: null descriptor", name);
-  if (A->format != NACHO_CSR && A->format != NACHO_DCSR) return fail(NACHO_ERR_INVALID_ARG, "%s: bad format %d", name, A->format);
+  if (A->format != NACHO_CSR && A->format != NACHO_DCSR && A->format != NACHO_COO)
+    return fail(NACHO_ERR_INVALID_ARG, "%s: bad format %d", name, A->format);
+  if (A->format == NACHO_COO && (A->nouter != 1 || (A->nnz > 0 && !A->outer_crd)))
+    return fail(NACHO_ERR_SHAPE, "%s: COO needs nouter == 1 (pos = [0, nnz]) and a row level", name);
   if (A->dtype != NACHO_F32 && A->dtype != NACHO_F64) return fail(NACHO_ERR_INVALID_ARG, "%s: bad dtype %d", name, A->dtype);
   if (A->nrows < 0 || A->ncols < 0 || A->nnz < 0 || A->nouter < 0) return fail(NACHO_ERR_SHAPE, "%s: negative size", name);
   if (A->ncols > INT32_MAX) return fail(NACHO_ERR_OVERFLOW, "%s: ncols %lld > INT32_MAX", name, (long long)A->ncols);
@@ -111,12 +114,18 @@ nacho_status check_ops(const nacho_matrix* ops, int32_t k) {
   if (k < 1 || k > NACHO_MAX_K) return fail(NACHO_ERR_INVALID_ARG, "k = %d outside [1, %d]", k, NACHO_MAX_K);
   for (int o = 0; o < k; ++o) {
     NACHO_TRY(check_matrix(ops + o, "operand"));
-    if (ops[o].format != ops[0].format || ops[o].nrows != ops[0].nrows || ops[o].ncols != ops[0].ncols ||
-        ops[o].dtype != ops[0].dtype)
+    const bool dense_rows = ops[o].format != NACHO_DCSR && ops[0].format != NACHO_DCSR;   // CSR / COO mix
+    if ((ops[o].format != ops[0].format && !dense_rows) || ops[o].nrows != ops[0].nrows ||
+        ops[o].ncols != ops[0].ncols || ops[o].dtype != ops[0].dtype)
       return fail(NACHO_ERR_SHAPE, "operand %d disagrees with operand 0 in format/shape/dtype", o);
   }
   if (ops[0].format == NACHO_DCSR && k > 4) return fail(NACHO_ERR_INVALID_ARG, "DCSR partitioning supports k <= 4");
   return NACHO_SUCCESS;
+}
+
+bool all_csr(const nacho_matrix* ops, int32_t k) {
+  for (int o = 0; o < k; ++o) if (ops[o].format != NACHO_CSR) return false;
+  return true;
 }
 
 OpsArg make_ops(const nacho_matrix* ops, int32_t k) {
@@ -130,7 +139,8 @@ OpsArg make_ops(const nacho_matrix* ops, int32_t k) {
     a.op[o].pos = ops[o].pos;
     a.op[o].crd = ops[o].crd;
     a.op[o].val = ops[o].val;
-    a.op[o].outer = ops[o].format == NACHO_DCSR ? ops[o].outer_crd : nullptr;
+    a.op[o].fmt = ops[o].format;
+    a.op[o].outer = ops[o].format != NACHO_CSR ? ops[o].outer_crd : nullptr;
     a.op[o].nouter = ops[o].nouter;
     a.op[o].nnz = ops[o].nnz;
   }
@@ -187,15 +197,19 @@ nacho_status launch_partition(const nacho_matrix* ops, int32_t k, const PartsArg
   const OpsArg a = make_ops(ops, k);
   if (Ptot < 0) Ptot = pa.P;
   const int64_t q = total_cost(ops, k);
+  bool levels = ops[0].format == NACHO_DCSR && k > 1;
+  for (int o = 0; o < k; ++o) levels = levels || ops[o].format == NACHO_COO;
+  if (levels) {   // k compressed / COO outer levels (dcsr_add.cuh)
+    if (Ptot != pa.P || p0 != 0) return fail(NACHO_ERR_INVALID_ARG, "partition slices take CSR (or one DCSR) operands");
+    if (k > 4) return fail(NACHO_ERR_INVALID_ARG, "DCSR / COO partitioning takes k <= 4 operands");
+    const unsigned g = (unsigned)((int64_t(pa.P) + 4) / 4);
+    if (k <= 2) dcsr_partition_kernel<2><<<g, 128, 0, st>>>(a, pa, q);
+    else dcsr_partition_kernel<4><<<g, 128, 0, st>>>(a, pa, q);
+    return launched("dcsr_partition_kernel");
+  }
   if (k == 1) {
     partition1_kernel<<<(unsigned)((int64_t(pa.P) + 256) / 256), 256, 0, st>>>(a, pa, q, Ptot, p0);
     return launched("partition1_kernel");
-  }
-  if (ops[0].format == NACHO_DCSR) {   // k compressed outer levels (dcsr_add.cuh)
-    const unsigned g = (unsigned)((int64_t(pa.P) + 4) / 4);
-    if (k == 2) dcsr_partition_kernel<2><<<g, 128, 0, st>>>(a, pa, q);
-    else dcsr_partition_kernel<4><<<g, 128, 0, st>>>(a, pa, q);
-    return launched("dcsr_partition_kernel");
   }
   const int64_t nb = (int64_t(pa.P) + 1 + kPartWarps - 1) / kPartWarps;
   if (k == 2) partition_kernel<kPartWarps, 2><<<(unsigned)nb, kPartWarps * 32, 0, st>>>(a, pa, q, Ptot, p0);
@@ -615,7 +629,7 @@ extern "C" {
 /* ------------------------------------------------------------------ k-way intersection (spadd7, OP) */
 static nacho_status check_intersection(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, cudaStream_t st) {
   NACHO_TRY(check_ops(ops, k));
-  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "intersection kernels take CSR operands");
+  if (!all_csr(ops, k)) return fail(NACHO_ERR_INVALID_ARG, "intersection kernels take CSR operands");
   if (k > 4) return fail(NACHO_ERR_INVALID_ARG, "intersection kernels take k <= 4 operands (k = %d)", k);
   NACHO_TRY(check_parts(parts, k));
   if (!spadd5_applies(ops, k, parts_arg(parts), st))
@@ -815,6 +829,45 @@ nacho_status nacho_dcsr_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_
   NACHO_TRY(launched("dcsr_spadd_kernel<1>"));
   rec_counts_kernel<<<1, 32, 0, st>>>(off_r + P, off_e + P, counts);
   return launched("rec_counts_kernel");
+}
+
+/* ------------------------------------------------------------------ mixed CSR / COO k-way SpAdd */
+size_t nacho_mixed_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t P) {
+  (void)ops; (void)k;
+  const size_t Pe = P > 0 ? P : 1;
+  return align_up((Pe + 1) * 8) + align_up((Pe + 2) * 8);
+}
+
+nacho_status nacho_mixed_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* nnz_z,
+                                 int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes, void* stream) {
+  NACHO_TRY(check_ops(ops, k));
+  if (k > 4) return fail(NACHO_ERR_INVALID_ARG, "nacho_mixed_spadd_k takes k <= 4 operands");
+  for (int o = 0; o < k; ++o)
+    if (ops[o].format == NACHO_DCSR) return fail(NACHO_ERR_INVALID_ARG, "nacho_mixed_spadd_k takes CSR / COO operands");
+  NACHO_TRY(check_parts(parts, k));
+  if (!nnz_z || !z_pos) return fail(NACHO_ERR_INVALID_ARG, "null output");
+  if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
+  const int64_t P = parts->P;
+  const size_t need = nacho_mixed_spadd_k_workspace_size(ops, k, parts->P);
+  if (!ws || ws_bytes < need) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t* cnt = static_cast<int64_t*>(ws);
+  int64_t* off = reinterpret_cast<int64_t*>(static_cast<char*>(ws) + align_up((P + 1) * 8));
+  const OpsArg a = make_ops(ops, k);
+  const PartsArg pa = parts_arg(parts);
+  const unsigned g = (unsigned)((P + 127) / 128);
+  const bool f64 = ops[0].dtype == NACHO_F64;
+  if (f64) mixed_spadd_kernel<double, 0><<<g, 128, 0, st>>>(a, pa, cnt, nullptr, nullptr, nullptr, nullptr);
+  else mixed_spadd_kernel<float, 0><<<g, 128, 0, st>>>(a, pa, cnt, nullptr, nullptr, nullptr, nullptr);
+  NACHO_TRY(launched("mixed_spadd_kernel<0>"));
+  rec_scan_kernel<1024><<<1, 1024, 0, st>>>(cnt, nullptr, P, off);
+  NACHO_TRY(launched("rec_scan_kernel"));
+  if (f64) mixed_spadd_kernel<double, 1><<<g, 128, 0, st>>>(a, pa, nullptr, off, z_pos, z_crd, static_cast<double*>(z_val));
+  else mixed_spadd_kernel<float, 1><<<g, 128, 0, st>>>(a, pa, nullptr, off, z_pos, z_crd, static_cast<float*>(z_val));
+  NACHO_TRY(launched("mixed_spadd_kernel<1>"));
+  if (cudaMemcpyAsync(nnz_z, off + P, 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return fail(NACHO_ERR_CUDA, "nnz_Z copy");
+  return NACHO_SUCCESS;
 }
 
 /* ------------------------------------------------------------------ multi-GPU (dist.cuh) */
@@ -1057,6 +1110,7 @@ size_t nacho_spmv_workspace_size(const nacho_matrix* A, int32_t P) {
 nacho_status nacho_spmv(const nacho_matrix* A, const nacho_parts* parts, const void* x, void* y, int32_t dense_y,
                         void* ws, size_t ws_bytes, void* stream) {
   NACHO_TRY(check_matrix(A, "A"));
+  if (A->format == NACHO_COO) return fail(NACHO_ERR_INVALID_ARG, "SpMV takes CSR / DCSR operands");
   if (!x && A->ncols > 0) return fail(NACHO_ERR_INVALID_ARG, "null x");
   if (!y && (A->nouter > 0 || (dense_y && A->nrows > 0))) return fail(NACHO_ERR_INVALID_ARG, "null y");
   if (parts) NACHO_TRY(check_parts(parts, 1));
@@ -1089,7 +1143,7 @@ size_t nacho_spadd_k_workspace_size(const nacho_matrix* ops, int32_t k, int32_t 
 nacho_status nacho_spadd_k_count(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
                                  void* ws, size_t ws_bytes, void* stream) {
   NACHO_TRY(check_ops(ops, k));
-  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands");
+  if (!all_csr(ops, k)) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands (COO: nacho_mixed_spadd_k)");
   NACHO_TRY(check_parts(parts, k));
   if (!part_off) return fail(NACHO_ERR_INVALID_ARG, "null part_off");
   const size_t need = nacho_spadd_k_workspace_size(ops, k, parts->P);
@@ -1120,7 +1174,7 @@ nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_
                                 size_t ws_bytes, void* stream) {
   (void)ws; (void)ws_bytes;
   NACHO_TRY(check_ops(ops, k));
-  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands");
+  if (!all_csr(ops, k)) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands (COO: nacho_mixed_spadd_k)");
   NACHO_TRY(check_parts(parts, k));
   if (!part_off || !z_pos) return fail(NACHO_ERR_INVALID_ARG, "null part_off / z_pos");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1147,7 +1201,7 @@ nacho_status nacho_spadd_k_fill(const nacho_matrix* ops, int32_t k, const nacho_
 nacho_status nacho_spadd_k(const nacho_matrix* ops, int32_t k, const nacho_parts* parts, int64_t* part_off,
                            int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes, void* stream) {
   NACHO_TRY(check_ops(ops, k));
-  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands");
+  if (!all_csr(ops, k)) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands (COO: nacho_mixed_spadd_k)");
   NACHO_TRY(check_parts(parts, k));
   if (!z_pos) return fail(NACHO_ERR_INVALID_ARG, "null z_pos");
   if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
@@ -1193,7 +1247,7 @@ nacho_status nacho_spadd_k_staged(const nacho_matrix* ops, int32_t k, const nach
                                   int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes,
                                   void* stream) {
   NACHO_TRY(check_ops(ops, k));
-  if (ops[0].format != NACHO_CSR) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands");
+  if (!all_csr(ops, k)) return fail(NACHO_ERR_INVALID_ARG, "SpAdd supports CSR operands (COO: nacho_mixed_spadd_k)");
   NACHO_TRY(check_parts(parts, k));
   if (!z_pos || !part_off) return fail(NACHO_ERR_INVALID_ARG, "null z_pos / part_off");
   if (total_cost(ops, k) > 0 && (!z_crd || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
@@ -1262,6 +1316,7 @@ nacho_status nacho_spmm(const nacho_matrix* A, const nacho_parts* parts, const v
 
 nacho_status nacho_validate(const nacho_matrix* A, void* stream) {
   NACHO_TRY(check_matrix(A, "A"));
+  if (A->format == NACHO_COO) return fail(NACHO_ERR_INVALID_ARG, "nacho_validate takes CSR / DCSR operands");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int* flag = nullptr;
   if (cudaMallocAsync(&flag, sizeof(int), st) != cudaSuccess) return fail(NACHO_ERR_CUDA, "cudaMallocAsync");

@@ -14,6 +14,7 @@ constexpr unsigned kFull = 0xffffffffu;
 // One sparse operand as the kernels see it: pos in the outer-position space
 // [0, nouter], crd/val in position space.  outer != nullptr <=> DCSR.
 struct OpView {
+  int32_t fmt;            // nacho_format: CSR, DCSR (outer = stored rows), COO (outer = row of every entry)
   const int64_t* pos;
   const int32_t* crd;
   const void* val;

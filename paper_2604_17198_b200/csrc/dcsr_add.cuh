@@ -38,12 +38,19 @@ __global__ void __launch_bounds__(128) dcsr_partition_kernel(const __grid_consta
     set_origin(a, b);
   } else if (p == out.P || Q >= qstar) {
     set_end(a, b);
+    if (a.op[0].fmt != NACHO_DCSR) b.row_pos = a.nrows;   // CSR / COO: the dense row index
   } else {
-    auto cost_ok = [&](int64_t x) {
+    auto cost_ok = [&](int64_t x) {   // C_i(x): entries of rows < x over the operands (per level type)
       int64_t s = 0;
 #pragma unroll
-      for (int o = 0; o < KM; ++o)
-        if (o < k) s += ldg(a.op[o].pos + dcsr_lb(a.op[o].outer, a.op[o].nouter, x));
+      for (int o = 0; o < KM; ++o) {
+        if (o < k) {
+          const OpView& op = a.op[o];
+          s += op.fmt == NACHO_CSR ? ldg(op.pos + x)
+             : op.fmt == NACHO_DCSR ? ldg(op.pos + dcsr_lb(op.outer, op.nouter, x))
+                                    : dcsr_lb(op.outer, op.nnz, x);   // COO: the row level per entry
+        }
+      }
       return s <= Q;
     };
     const int64_t x = warp_highest_true(0, a.nrows, cost_ok);
@@ -52,16 +59,25 @@ __global__ void __launch_bounds__(128) dcsr_partition_kernel(const __grid_consta
 #pragma unroll
     for (int o = 0; o < KM; ++o) {
       if (o < k) {
-        const int64_t i = dcsr_lb(a.op[o].outer, a.op[o].nouter, x);
-        const bool present = i < a.op[o].nouter && (int64_t)ldg(a.op[o].outer + i) == x;
-        lo[o] = ldg(a.op[o].pos + i);
-        hi[o] = present ? ldg(a.op[o].pos + i + 1) : lo[o];
+        const OpView& op = a.op[o];
+        if (op.fmt == NACHO_CSR) {
+          lo[o] = ldg(op.pos + x);
+          hi[o] = ldg(op.pos + x + 1);
+        } else if (op.fmt == NACHO_DCSR) {
+          const int64_t i = dcsr_lb(op.outer, op.nouter, x);
+          const bool present = i < op.nouter && (int64_t)ldg(op.outer + i) == x;
+          lo[o] = ldg(op.pos + i);
+          hi[o] = present ? ldg(op.pos + i + 1) : lo[o];
+        } else {
+          lo[o] = dcsr_lb(op.outer, op.nnz, x);
+          hi[o] = dcsr_lb(op.outer, op.nnz, x + 1);
+        }
         R -= lo[o];
       }
     }
     warp_kway_select<KM>(a, k, lo, hi, R, b);
     b.row = x;
-    b.row_pos = dcsr_lb(a.op[0].outer, a.op[0].nouter, x);
+    b.row_pos = a.op[0].fmt == NACHO_DCSR ? dcsr_lb(a.op[0].outer, a.op[0].nouter, x) : x;
   }
   if (lane == 0) {
     out.query[p] = Q;
@@ -155,6 +171,61 @@ __global__ void __launch_bounds__(128) dcsr_spadd_kernel(const __grid_constant__
     if (done) z_pos[ri + 1] = e0 + ne;
   }
   if (!MODE) { ent[p] = ne; rst[p] = nr; }
+}
+
+// k-way union of CSR and COO operands mixed (the COO + CSR addition), Z in CSR: one
+// thread per partition walks its rows [b_p.row, b_{p+1}.row] (the last one up to the cut): an
+// operand's entries of row r inside the partition are [max(pos[r], s_o), min(pos[r + 1], e_o)) for
+// CSR and the run of its row level equal to r from its cursor for COO.  MODE 0 counts; MODE 1 writes
+// Z at off[p] and Z.pos[r + 1] of every row the partition owns (R7: r < b_{p+1}.row).
+template <typename V, int MODE>
+__global__ void __launch_bounds__(128) mixed_spadd_kernel(const __grid_constant__ OpsArg a, PartsArg pa, int64_t* cnt,
+                                                          const int64_t* off, int64_t* z_pos, int32_t* z_crd,
+                                                          V* z_val) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= pa.P) return;
+  const int k = a.k;
+  const int64_t M = a.nrows;
+  const int64_t r0 = pa.row[p], r1 = pa.row[p + 1];
+  int64_t q[NACHO_MAX_K], e[NACHO_MAX_K];
+  for (int o = 0; o < k; ++o) { q[o] = pa.pos[p * k + o]; e[o] = pa.pos[(p + 1) * k + o]; }
+  int64_t n = 0;
+  const int64_t w0 = MODE ? off[p] : 0;
+  if (MODE && p == 0) z_pos[0] = 0;
+  for (int64_t r = r0; r <= r1 && r < M; ++r) {
+    int64_t hi[NACHO_MAX_K];
+    for (int o = 0; o < k; ++o) {
+      const OpView& op = a.op[o];
+      if (op.fmt == NACHO_CSR) {
+        const int64_t rs = ldg(op.pos + r), re = ldg(op.pos + r + 1);
+        if (q[o] < rs) q[o] = rs;
+        hi[o] = re < e[o] ? re : e[o];
+      } else {
+        int64_t h = q[o];
+        while (h < e[o] && (int64_t)ldg(op.outer + h) == r) ++h;
+        hi[o] = h;
+      }
+    }
+    for (;;) {
+      int32_t j = INT32_MAX;
+      for (int o = 0; o < k; ++o) if (q[o] < hi[o]) j = min(j, ldg(a.op[o].crd + q[o]));
+      if (j == INT32_MAX) break;
+      V acc = V(0);
+      bool have = false;
+      for (int o = 0; o < k; ++o) {
+        if (q[o] < hi[o] && ldg(a.op[o].crd + q[o]) == j) {
+          const V x = static_cast<const V*>(a.op[o].val)[q[o]];
+          acc = have ? acc + x : x;
+          have = true;
+          ++q[o];
+        }
+      }
+      if (MODE) { z_crd[w0 + n] = j; z_val[w0 + n] = acc; }
+      ++n;
+    }
+    if (MODE && r < r1) z_pos[r + 1] = w0 + n;   // owned row (R7)
+  }
+  if (!MODE) cnt[p] = n;
 }
 
 }  // namespace nacho

@@ -204,9 +204,14 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_kernel(SpmmArgs<T> a) {
 constexpr int kSm2Groups = 32;       // 8-lane groups per CTA (256 threads)
 constexpr int kSm2Items = 32;        // positions per group
 constexpr int kSm2Tile = kSm2Groups * kSm2Items;
+#ifndef NACHO_SM2_BATCH   // nonzeros whose B rows a lane group loads before using them (registers: 8 per nonzero)
+#define NACHO_SM2_BATCH 4
+#define NACHO_SM2_MINB 3
+#endif
+constexpr int kSm2Batch = NACHO_SM2_BATCH;
 
 template <bool CHUNKED>
-__global__ void __launch_bounds__(256, 3) spmm64_kernel(const __grid_constant__ SpmmArgs<float> a) {
+__global__ void __launch_bounds__(256, NACHO_SM2_MINB) spmm64_kernel(const __grid_constant__ SpmmArgs<float> a) {
   __shared__ float4 s_tail[kSm2Groups][16];   // 64 floats per group
   __shared__ int64_t s_tkey[kSm2Groups];
   const int tid = threadIdx.x, g = tid >> 3, gl = tid & 7;
@@ -276,13 +281,13 @@ __global__ void __launch_bounds__(256, 3) spmm64_kernel(const __grid_constant__ 
       mv[u] = j < cnt ? ldg(a.val + at + j) : 0.f;
     }
 #pragma unroll
-    for (int ib = 0; ib < kSm2Items / 4; ++ib) {   // batches of 4 positions (static register indices)
-      if (4 * ib >= cnt) break;
-      float4 b0[4], b1[4];
-      float vv[4];
+    for (int ib = 0; ib < kSm2Items / kSm2Batch; ++ib) {   // batches of positions (static register indices)
+      if (kSm2Batch * ib >= cnt) break;
+      float4 b0[kSm2Batch], b1[kSm2Batch];
+      float vv[kSm2Batch];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = 4 * ib + u;
+      for (int u = 0; u < kSm2Batch; ++u) {
+        const int j = kSm2Batch * ib + u;
         const int32_t c = __shfl_sync(gmask, mc[j >> 3], j & 7, 8);
         vv[u] = __shfl_sync(gmask, mv[j >> 3], j & 7, 8);
         if (j < cnt) {
@@ -292,8 +297,8 @@ __global__ void __launch_bounds__(256, 3) spmm64_kernel(const __grid_constant__ 
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = 4 * ib + u;
+      for (int u = 0; u < kSm2Batch; ++u) {
+        const int j = kSm2Batch * ib + u;
         if (j < cnt) {
           const int64_t q = at + j;
           while (next_end <= q) {
