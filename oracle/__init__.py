@@ -74,6 +74,10 @@ def lib():
         L.oracle_dcsr_spadd_counts.argtypes = [ctypes.c_int32, vp, vp, vp, vp]
         L.oracle_mixed_spadd_k.argtypes = [ctypes.c_int32, vp, vp, vp, vp, i64]
         L.oracle_mixed_spadd_k.restype = i64
+        L.oracle_csf_cost.argtypes = [ctypes.c_int32, vp, i64, i64, i64, vp, vp, vp]
+        L.oracle_csf_partition_rank.argtypes = [ctypes.c_int32, vp, ctypes.c_int32, vp]
+        L.oracle_csf_spadd_k.argtypes = [ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, vp]
+        L.oracle_csf_spadd_k.restype = i64
     return _lib
 
 
@@ -331,4 +335,60 @@ def mixed_spadd_k(ops):
     if n < 0:
         raise ValueError("oracle_mixed_spadd_k failed (CSR / COO operands only)")
     return z_pos, z_crd[:n].copy(), z_val[:n].copy()
+
+
+# ------------------------------------------------------------------ third-order CSF
+class _Tensor3(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int32), ("n0", ctypes.c_int64), ("n1", ctypes.c_int64), ("n2", ctypes.c_int64),
+                ("nnz", ctypes.c_int64), ("n_slices", ctypes.c_int64), ("n_fibers", ctypes.c_int64),
+                ("crd0", ctypes.c_void_p), ("pos1", ctypes.c_void_p), ("crd1", ctypes.c_void_p),
+                ("pos2", ctypes.c_void_p), ("crd2", ctypes.c_void_p), ("val", ctypes.c_void_p)]
+
+
+def _tensors(ops):
+    keep = []
+    arr = (_Tensor3 * len(ops))()
+    for i, T in enumerate(ops):
+        a = [np.ascontiguousarray(x, dtype=d) for x, d in
+             ((T.crd0, np.int32), (T.pos1, np.int64), (T.crd1, np.int32), (T.pos2, np.int64), (T.crd2, np.int32))]
+        val = np.ascontiguousarray(T.val)
+        keep += a + [val]
+        arr[i].dtype = 1 if val.dtype == np.float64 else 0
+        arr[i].n0, arr[i].n1, arr[i].n2 = T.shape
+        arr[i].nnz, arr[i].n_slices, arr[i].n_fibers = a[4].shape[0], a[0].shape[0], a[2].shape[0]
+        arr[i].crd0, arr[i].pos1, arr[i].crd1, arr[i].pos2, arr[i].crd2 = (_p(x) for x in a)
+        arr[i].val = _p(val)
+    return arr, keep
+
+
+def csf_cost(ops, xi, xj, xk):
+    arr, keep = _tensors(ops)
+    c = [ctypes.c_int64(0) for _ in range(3)]
+    lib().oracle_csf_cost(len(ops), arr, xi, xj, xk, *(ctypes.byref(x) for x in c))
+    return tuple(int(x.value) for x in c)
+
+
+def csf_partition_rank(ops, P) -> Parts:
+    arr, keep = _tensors(ops)
+    out = Parts(P, len(ops))
+    s = out.c()
+    if lib().oracle_csf_partition_rank(len(ops), arr, P, ctypes.byref(s)) != 0:
+        raise ValueError("oracle_csf_partition_rank failed")
+    return out
+
+
+def csf_spadd_k(ops):
+    """(crd0, pos1, crd1, pos2, crd2, val) of the 3-level union Z = sum_o ops[o] in CSF."""
+    arr, keep = _tensors(ops)
+    cs = max(1, sum(len(T.crd0) for T in ops))
+    cf = max(1, sum(len(T.crd1) for T in ops))
+    ce = max(1, sum(len(T.crd2) for T in ops))
+    z = [np.zeros(cs, np.int32), np.zeros(cs + 1, np.int64), np.zeros(cf, np.int32), np.zeros(cf + 1, np.int64),
+         np.zeros(ce, np.int32), np.zeros(ce, dtype=np.asarray(ops[0].val).dtype)]
+    counts = np.zeros(3, np.int64)
+    n = lib().oracle_csf_spadd_k(len(ops), arr, *(_p(x) for x in z), cs, cf, ce, _p(counts))
+    if n < 0:
+        raise ValueError("oracle_csf_spadd_k overflow")
+    ns, nf, ne = (int(x) for x in counts)
+    return z[0][:ns], z[1][:ns + 1], z[2][:nf], z[3][:nf + 1], z[4][:ne], z[5][:ne]
 

@@ -744,3 +744,135 @@ int64_t oracle_mixed_spadd_k(int32_t k, const or_matrix *ops, int64_t *z_pos, in
     return nz;
 }
 
+/* ------------------------------------------------------ third-order CSF (3-level Alg. 1) */
+static int64_t lb32(const int32_t *a, int64_t lo, int64_t hi, int64_t x) {   /* least i in [lo, hi] with a[i] >= x */
+    while (lo < hi) { int64_t m = lo + (hi - lo) / 2; if ((int64_t)a[m] >= x) hi = m; else lo = m + 1; }
+    return lo;
+}
+
+/* C_i(x_i) = entries of slices i < x_i; C_j(x_j | x_i) = entries of slice x_i in fibers j < x_j;
+ * C_k(x_k | x_i, x_j) = entries of fiber (x_i, x_j) with k < x_k -- summed over the operands
+ * (the nnz cost functions of P:1689 on the levels of fig:coordinate-tree). */
+void oracle_csf_cost(int32_t k, const or_tensor3 *ops, int64_t xi, int64_t xj, int64_t xk, int64_t *ci, int64_t *cj,
+                     int64_t *ck) {
+    *ci = *cj = *ck = 0;
+    for (int32_t o = 0; o < k; o++) {
+        const or_tensor3 *T = &ops[o];
+        const int64_t s = lb32(T->crd0, 0, T->n_slices, xi);
+        *ci += T->pos2[T->pos1[s]];
+        if (s < T->n_slices && T->crd0[s] == xi) {
+            const int64_t f = lb32(T->crd1, T->pos1[s], T->pos1[s + 1], xj);
+            *cj += T->pos2[f] - T->pos2[T->pos1[s]];
+            if (f < T->pos1[s + 1] && T->crd1[f] == xj)
+                *ck += lb32(T->crd2, T->pos2[f], T->pos2[f + 1], xk) - T->pos2[f];
+        }
+    }
+}
+
+/* The entries of every operand enumerated in lexicographic (i, j, k) order by a 3-level k-finger
+ * merge (Listing 1's union form); b_p = entry number Q_p (R1-R4 as in oracle_partition_rank). */
+int oracle_csf_partition_rank(int32_t k, const or_tensor3 *ops, int32_t P, or_parts *out) {
+    if (k < 1 || P < 1) return 1;
+    int64_t qstar = 0;
+    for (int32_t o = 0; o < k; o++) qstar += ops[o].nnz;
+    oracle_queries(qstar, P, out->query);
+    int64_t *q = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t *f = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t *sl = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t c = 0;
+    int32_t p = 1;
+    while (p < P) {
+        int64_t bi = -1, bj = -1, bk = -1;
+        for (int32_t o = 0; o < k; o++) {
+            if (q[o] >= ops[o].nnz) continue;
+            while (ops[o].pos2[f[o] + 1] <= q[o]) f[o]++;
+            while (ops[o].pos1[sl[o] + 1] <= f[o]) sl[o]++;
+            const int64_t i = ops[o].crd0[sl[o]], j = ops[o].crd1[f[o]], kk = ops[o].crd2[q[o]];
+            if (bi < 0 || i < bi || (i == bi && (j < bj || (j == bj && kk < bk)))) { bi = i; bj = j; bk = kk; }
+        }
+        if (bi < 0) break;
+        int32_t g = 0;
+        for (int32_t o = 0; o < k; o++)
+            if (q[o] < ops[o].nnz && ops[o].crd0[sl[o]] == bi && ops[o].crd1[f[o]] == bj && ops[o].crd2[q[o]] == bk) g++;
+        while (p < P && out->query[p] < c + g) {
+            out->row[p] = bi; out->row_pos[p] = bj; out->col[p] = (int32_t)bk;
+            for (int32_t o = 0; o < k; o++) out->pos[(int64_t)p * k + o] = q[o];
+            p++;
+        }
+        for (int32_t o = 0; o < k; o++)
+            if (q[o] < ops[o].nnz && ops[o].crd0[sl[o]] == bi && ops[o].crd1[f[o]] == bj && ops[o].crd2[q[o]] == bk) q[o]++;
+        c += g;
+    }
+    for (; p <= P; p++) {   /* end: (n0, 0, 0), every operand exhausted */
+        out->row[p] = ops[0].n0; out->row_pos[p] = 0; out->col[p] = 0;
+        for (int32_t o = 0; o < k; o++) out->pos[(int64_t)p * k + o] = ops[o].nnz;
+    }
+    out->row[0] = 0; out->row_pos[0] = 0; out->col[0] = 0;
+    for (int32_t o = 0; o < k; o++) out->pos[o] = 0;
+    free(q); free(f); free(sl);
+    return 0;
+}
+
+/* Z = sum_o A_o, three nested union loops (Listing 2 with one more level), left fold (R9). */
+int64_t oracle_csf_spadd_k(int32_t k, const or_tensor3 *ops, int32_t *z_crd0, int64_t *z_pos1, int32_t *z_crd1,
+                           int64_t *z_pos2, int32_t *z_crd2, void *z_val, int64_t cap_s, int64_t cap_f, int64_t cap_e,
+                           int64_t *counts) {
+    const int f64 = ops[0].dtype == OR_F64;
+    int64_t *s = (int64_t *)calloc((size_t)k, sizeof(int64_t));   /* slice cursors */
+    int64_t *f = (int64_t *)calloc((size_t)k, sizeof(int64_t)), *fe = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t *q = (int64_t *)calloc((size_t)k, sizeof(int64_t)), *qe = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    int64_t ns = 0, nf = 0, ne = 0;
+    z_pos1[0] = 0; z_pos2[0] = 0;
+    for (;;) {
+        int64_t i = -1;
+        for (int32_t o = 0; o < k; o++) if (s[o] < ops[o].n_slices && (i < 0 || ops[o].crd0[s[o]] < i)) i = ops[o].crd0[s[o]];
+        if (i < 0) break;
+        for (int32_t o = 0; o < k; o++) {
+            if (s[o] < ops[o].n_slices && ops[o].crd0[s[o]] == i) { f[o] = ops[o].pos1[s[o]]; fe[o] = ops[o].pos1[s[o] + 1]; }
+            else { f[o] = fe[o] = 0; }
+        }
+        for (;;) {
+            int64_t j = -1;
+            for (int32_t o = 0; o < k; o++) if (f[o] < fe[o] && (j < 0 || ops[o].crd1[f[o]] < j)) j = ops[o].crd1[f[o]];
+            if (j < 0) break;
+            for (int32_t o = 0; o < k; o++) {
+                if (f[o] < fe[o] && ops[o].crd1[f[o]] == j) { q[o] = ops[o].pos2[f[o]]; qe[o] = ops[o].pos2[f[o] + 1]; }
+                else { q[o] = qe[o] = 0; }
+            }
+            for (;;) {
+                int64_t kk = -1;
+                for (int32_t o = 0; o < k; o++) if (q[o] < qe[o] && (kk < 0 || ops[o].crd2[q[o]] < kk)) kk = ops[o].crd2[q[o]];
+                if (kk < 0) break;
+                double vd = 0.0; float vf = 0.0f; int have = 0;
+                for (int32_t o = 0; o < k; o++) {
+                    if (q[o] < qe[o] && ops[o].crd2[q[o]] == kk) {
+                        if (f64) { double a = ((const double *)ops[o].val)[q[o]]; vd = have ? vd + a : a; }
+                        else     { float  a = ((const float *)ops[o].val)[q[o]];  vf = have ? vf + a : a; }
+                        have = 1; q[o]++;
+                    }
+                }
+                if (ne >= cap_e) goto overflow;
+                z_crd2[ne] = (int32_t)kk;
+                if (f64) ((double *)z_val)[ne] = vd; else ((float *)z_val)[ne] = vf;
+                ne++;
+            }
+            if (nf >= cap_f) goto overflow;
+            z_crd1[nf] = (int32_t)j;
+            z_pos2[nf + 1] = ne;
+            nf++;
+            for (int32_t o = 0; o < k; o++) if (f[o] < fe[o] && ops[o].crd1[f[o]] == j) f[o]++;
+        }
+        if (ns >= cap_s) goto overflow;
+        z_crd0[ns] = (int32_t)i;
+        z_pos1[ns + 1] = nf;
+        ns++;
+        for (int32_t o = 0; o < k; o++) if (s[o] < ops[o].n_slices && ops[o].crd0[s[o]] == i) s[o]++;
+    }
+    counts[0] = ns; counts[1] = nf; counts[2] = ne;
+    free(s); free(f); free(fe); free(q); free(qe);
+    return ne;
+overflow:
+    free(s); free(f); free(fe); free(q); free(qe);
+    return -1;
+}
+

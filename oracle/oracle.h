@@ -106,6 +106,33 @@ int     oracle_dcsr_spadd_counts(int32_t k, const or_matrix *ops, const or_parts
 int64_t oracle_mixed_spadd_k(int32_t k, const or_matrix *ops, int64_t *z_pos, int32_t *z_crd, void *z_val,
                              int64_t capacity);
 
+/* A third-order tensor in CSF (Compressed o Compressed o Compressed, P:846-1030 coordinate tree):
+ * slices crd0[n_slices] (i), fibers pos1[n_slices+1] / crd1[n_fibers] (j), entries pos2[n_fibers+1] /
+ * crd2[nnz] (k), val[nnz]. */
+typedef struct {
+    int32_t        dtype;
+    int64_t        n0, n1, n2, nnz, n_slices, n_fibers;
+    const int32_t *crd0;
+    const int64_t *pos1;
+    const int32_t *crd1;
+    const int64_t *pos2;
+    const int32_t *crd2;
+    const void    *val;
+} or_tensor3;
+
+/* The cost of coordinate (x_i, x_j, x_k) over k CSF operands: entries lexicographically before it,
+ * split as C_i(x_i) + C_j(x_j | x_i) + C_k(x_k | x_i, x_j) (fig:coordinate-tree). */
+void    oracle_csf_cost(int32_t k, const or_tensor3 *ops, int64_t xi, int64_t xj, int64_t xk, int64_t *ci, int64_t *cj,
+                        int64_t *ck);
+/* Partition boundaries of k CSF operands by the rank definition: row = i, row_pos = j, col = k,
+ * pos[o] = level-2 positions (entries of operand o before the boundary). */
+int     oracle_csf_partition_rank(int32_t k, const or_tensor3 *ops, int32_t P, or_parts *out);
+/* Z = sum_o ops[o] (3-level union, left fold) in CSF; counts[0..2] = slices, fibers, nnz.  -1 on
+ * capacity overflow. */
+int64_t oracle_csf_spadd_k(int32_t k, const or_tensor3 *ops, int32_t *z_crd0, int64_t *z_pos1, int32_t *z_crd1,
+                           int64_t *z_pos2, int32_t *z_crd2, void *z_val, int64_t cap_s, int64_t cap_f, int64_t cap_e,
+                           int64_t *counts);
+
 #ifdef __cplusplus
 }
 #endif

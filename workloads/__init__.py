@@ -363,3 +363,52 @@ def to_coo(A: SparseMatrix) -> SparseMatrix:
         pos = torch.tensor([0, A.nnz], dtype=torch.int64, device=A.pos.device)
     return SparseMatrix(COO, A.nrows, A.ncols, pos, A.crd, A.val, rows)
 
+
+@dataclass
+class Tensor3:
+    """A third-order tensor in CSF (Compressed o Compressed o Compressed): slices crd0 (i), fibers
+    pos1 / crd1 (j), entries pos2 / crd2 (k), val."""
+    shape: tuple
+    crd0: object
+    pos1: object
+    crd1: object
+    pos2: object
+    crd2: object
+    val: object
+
+    @property
+    def nnz(self) -> int:
+        return int(self.crd2.shape[0])
+
+    def to(self, device) -> "Tensor3":
+        import torch
+
+        def cv(a):
+            return a if isinstance(a, torch.Tensor) and a.device == torch.device(device) else torch.as_tensor(a).to(device)
+        return Tensor3(self.shape, cv(self.crd0), cv(self.pos1), cv(self.crd1), cv(self.pos2), cv(self.crd2), cv(self.val))
+
+
+def csf_from_coo(i, j, k, vals, shape, dtype=np.float32) -> Tensor3:
+    """A CSF tensor from coordinate lists (fixtures; duplicates not allowed)."""
+    i, j, k = (np.asarray(x, dtype=np.int64) for x in (i, j, k))
+    vals = np.asarray(vals, dtype=dtype)
+    order = np.lexsort((k, j, i))
+    i, j, k, vals = i[order], j[order], k[order], vals[order]
+    fib = np.ones(len(i), bool)
+    fib[1:] = (i[1:] != i[:-1]) | (j[1:] != j[:-1])
+    fstart = np.nonzero(fib)[0]
+    pos2 = np.concatenate([fstart, [len(i)]]).astype(np.int64)
+    fi, fj = i[fstart], j[fstart]
+    sl = np.ones(len(fi), bool)
+    sl[1:] = fi[1:] != fi[:-1]
+    sstart = np.nonzero(sl)[0]
+    pos1 = np.concatenate([sstart, [len(fi)]]).astype(np.int64)
+    return Tensor3(tuple(int(x) for x in shape), fi[sstart].astype(np.int32), pos1, fj.astype(np.int32), pos2,
+                   k.astype(np.int32), vals)
+
+
+def random_csf(rng, shape, density, dtype=np.float32) -> Tensor3:
+    mask = rng.random(shape) < density
+    i, j, k = np.nonzero(mask)
+    return csf_from_coo(i, j, k, rng.uniform(0.5, 1.5, len(i)), shape, dtype)
+
