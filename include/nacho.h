@@ -254,6 +254,46 @@ nacho_status nacho_mixed_spadd_k(const nacho_matrix* ops, int32_t k, const nacho
                                  int64_t* z_pos, int32_t* z_crd, void* z_val, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------------------------
+ * Third-order tensors in CSF = Compressed(i) o Compressed(j) o Compressed(k): the coordinate tree of
+ * fig:coordinate-tree.  crd0[n_slices] strictly increasing slice coordinates;
+ * pos1[n_slices + 1] fiber ranges, crd1[n_fibers] increasing within a slice; pos2[n_fibers + 1]
+ * entry ranges, crd2[nnz] increasing within a fiber; val[nnz].  Every stored slice / fiber non-empty,
+ * pos1[0] = pos2[0] = 0.  All arrays device memory, owned by the caller. */
+typedef struct {
+  int32_t dtype;   /* nacho_dtype of val */
+  int64_t n0, n1, n2;
+  int64_t nnz, n_slices, n_fibers;
+  const int32_t* crd0;
+  const int64_t* pos1;
+  const int32_t* crd1;
+  const int64_t* pos2;
+  const int32_t* crd2;
+  const void* val;
+} nacho_tensor3;
+
+/* nacho_partition_csf -- Alg. 1 at d = 3 for k CSF operands of one shape: boundary p is
+ * the highest coordinate (x_i, x_j, x_k) whose cost C_i(x_i) + C_j(x_j | x_i) + C_k(x_k | x_i, x_j)
+ * (the entries lexicographically before it, summed over the operands; the coordinate-tree cost
+ * functions) is <= Q_p = floor(p Q* / P), Q* = sum_o nnz_o.  One warp per
+ * boundary: a 32-ary search per level (i over [0, n0], j inside slice x_i) and the k-way select of
+ * the CSR path over the fibers' crd2 segments.  out->row = x_i, out->row_pos = x_j, out->col = x_k,
+ * out->pos[p k + o] = entries of operand o before b_p; b_0 = (0, 0, 0), b_P = (n0, 0, 0) with
+ * pos = nnz.  k <= 4.  Errors: INVALID_ARG (k, P, nulls), SHAPE (shapes differ). */
+nacho_status nacho_partition_csf(const nacho_tensor3* ops, int32_t k, int32_t P, nacho_parts* out, void* stream);
+
+/* nacho_csf_spadd_k -- Z = ops[0] + ... + ops[k-1] in CSF (the paper's third-order tensor addition,
+ * P:2403-2441) over the partition nacho_partition_csf made: assembly (entries, fibers
+ * and slices started per partition), three prefix sums, compute (one thread per partition, Listing 8's
+ * shape, the union at three levels; pos1 / pos2 written by the partition that completes the slice /
+ * fiber).  counts (device int64[3]) = Z's slices, fibers, nnz.  Capacities: z_crd0 / z_pos1 >= sum_o
+ * n_slices_o (+1), z_crd1 / z_pos2 >= sum_o n_fibers_o (+1), z_crd2 / z_val >= sum_o nnz_o.  Values fold
+ * left in operand order (R9).  k <= 4. */
+size_t nacho_csf_spadd_k_workspace_size(const nacho_tensor3* ops, int32_t k, int32_t P);
+nacho_status nacho_csf_spadd_k(const nacho_tensor3* ops, int32_t k, const nacho_parts* parts, int64_t* counts,
+                               int32_t* z_crd0, int64_t* z_pos1, int32_t* z_crd1, int64_t* z_pos2, int32_t* z_crd2,
+                               void* z_val, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
  * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.
  * Synchronous on `stream` (it reads one flag back).  Returns NACHO_ERR_FORMAT on a violation. */
 nacho_status nacho_validate(const nacho_matrix* A, void* stream);

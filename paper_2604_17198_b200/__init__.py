@@ -43,6 +43,13 @@ class PartsC(ctypes.Structure):
                 ("pos", ctypes.c_void_p), ("max_work", ctypes.c_int64)]
 
 
+class Tensor3C(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int32), ("n0", ctypes.c_int64), ("n1", ctypes.c_int64), ("n2", ctypes.c_int64),
+                ("nnz", ctypes.c_int64), ("n_slices", ctypes.c_int64), ("n_fibers", ctypes.c_int64),
+                ("crd0", ctypes.c_void_p), ("pos1", ctypes.c_void_p), ("crd1", ctypes.c_void_p),
+                ("pos2", ctypes.c_void_p), ("crd2", ctypes.c_void_p), ("val", ctypes.c_void_p)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() (no CPU fallback exists)")
@@ -83,6 +90,10 @@ def _load():
     L.nacho_mixed_spadd_k_workspace_size.argtypes = [vp, i32, i32]
     L.nacho_mixed_spadd_k_workspace_size.restype = sz
     L.nacho_mixed_spadd_k.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_partition_csf.argtypes = [vp, i32, i32, vp, vp]
+    L.nacho_csf_spadd_k_workspace_size.argtypes = [vp, i32, i32]
+    L.nacho_csf_spadd_k_workspace_size.restype = sz
+    L.nacho_csf_spadd_k.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     # multi-GPU (dist.cuh)
     L.nacho_dist_unique_id_size.restype = sz
     L.nacho_dist_unique_id.argtypes = [vp]
@@ -110,6 +121,7 @@ EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", 
            "nacho_launch_count", "nacho_hadamard_k", "nacho_inner_k_workspace_size", "nacho_inner_k",
            "nacho_dcsr_hadamard_workspace_size", "nacho_dcsr_hadamard", "nacho_dcsr_spadd_k_workspace_size",
            "nacho_dcsr_spadd_k", "nacho_mixed_spadd_k_workspace_size", "nacho_mixed_spadd_k",
+           "nacho_partition_csf", "nacho_csf_spadd_k_workspace_size", "nacho_csf_spadd_k",
            "nacho_dist_unique_id_size", "nacho_dist_unique_id", "nacho_dist_init",
            "nacho_dist_destroy", "nacho_dist_broadcast", "nacho_device_cuts", "nacho_shard_rows", "nacho_dist_seam",
            "nacho_dist_spmv_workspace_size", "nacho_dist_spmv", "nacho_dist_spadd_workspace_size",
@@ -440,6 +452,63 @@ def mixed_spadd_k(ops, parts: Parts, stream=None):
                                    _ptr(ws), need, _stream(stream)))
     n = int(nnz.item())
     return z_pos, z_crd[:n], z_val[:n]
+
+
+# ------------------------------------------------------------------ third-order CSF (include/nacho.h, csf.cuh)
+def tensor3(T) -> Tensor3C:
+    """nacho_tensor3 descriptor of a workloads.Tensor3-like object on the device (no copies)."""
+    for name, dt in (("crd0", torch.int32), ("pos1", torch.int64), ("crd1", torch.int32), ("pos2", torch.int64),
+                     ("crd2", torch.int32)):
+        _require(getattr(T, name), dt, name)
+    if T.val.dtype not in (torch.float32, torch.float64):
+        raise TypeError("val must be float32 or float64")
+    _require(T.val, T.val.dtype, "val")
+    s = Tensor3C()
+    s.dtype = NACHO_F64 if T.val.dtype == torch.float64 else NACHO_F32
+    s.n0, s.n1, s.n2 = (int(x) for x in T.shape)
+    s.nnz, s.n_slices, s.n_fibers = int(T.crd2.shape[0]), int(T.crd0.shape[0]), int(T.crd1.shape[0])
+    s.crd0, s.pos1, s.crd1 = T.crd0.data_ptr(), T.pos1.data_ptr(), T.crd1.data_ptr()
+    s.pos2, s.crd2, s.val = T.pos2.data_ptr(), T.crd2.data_ptr(), T.val.data_ptr()
+    return s
+
+
+def _tensors3(ops):
+    arr = (Tensor3C * len(ops))()
+    for i, T in enumerate(ops):
+        arr[i] = tensor3(T)
+    return arr
+
+
+def partition_csf(ops, P: int, stream=None) -> Parts:
+    """nacho_partition_csf: Alg. 1 at d = 3 (row = x_i, row_pos = x_j, col = x_k)."""
+    arr = _tensors3(ops)
+    out = Parts(P, len(ops), ops[0].pos1.device)
+    pc = out.c()
+    _check(lib.nacho_partition_csf(arr, len(ops), P, ctypes.byref(pc), _stream(stream)))
+    out.max_work = pc.max_work
+    return out
+
+
+def csf_spadd_k(ops, parts: Parts, stream=None):
+    """nacho_csf_spadd_k: Z = sum of CSF operands over `parts`.  Returns (crd0, pos1, crd1, pos2, crd2,
+    val) trimmed to Z's slices / fibers / nnz (one host read)."""
+    arr = _tensors3(ops)
+    dev = ops[0].pos1.device
+    k = len(ops)
+    cs = max(1, sum(int(T.crd0.shape[0]) for T in ops))
+    cf = max(1, sum(int(T.crd1.shape[0]) for T in ops))
+    ce = max(1, sum(int(T.crd2.shape[0]) for T in ops))
+    counts = torch.zeros(3, dtype=torch.int64, device=dev)
+    z = [torch.empty(cs, dtype=torch.int32, device=dev), torch.zeros(cs + 1, dtype=torch.int64, device=dev),
+         torch.empty(cf, dtype=torch.int32, device=dev), torch.zeros(cf + 1, dtype=torch.int64, device=dev),
+         torch.empty(ce, dtype=torch.int32, device=dev), torch.empty(ce, dtype=ops[0].val.dtype, device=dev)]
+    need = lib.nacho_csf_spadd_k_workspace_size(arr, k, parts.P)
+    ws, _ = _workspace(need, dev)
+    pc = parts.c()
+    _check(lib.nacho_csf_spadd_k(arr, k, ctypes.byref(pc), _ptr(counts), *(_ptr(x) for x in z), _ptr(ws), need,
+                                 _stream(stream)))
+    ns, nf, ne = (int(v) for v in counts.cpu().tolist())
+    return z[0][:ns], z[1][:ns + 1], z[2][:nf], z[3][:nf + 1], z[4][:ne], z[5][:ne]
 
 
 # ------------------------------------------------------------------ multi-GPU (include/nacho.h, dist.cuh)

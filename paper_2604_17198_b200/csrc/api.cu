@@ -19,6 +19,7 @@
 #include "dist.cuh"
 #include "recursive.cuh"
 #include "dcsr_add.cuh"
+#include "csf.cuh"
 #include "spmm.cuh"
 #include "spmv.cuh"
 #include "spmv3.cuh"
@@ -868,6 +869,93 @@ nacho_status nacho_mixed_spadd_k(const nacho_matrix* ops, int32_t k, const nacho
   if (cudaMemcpyAsync(nnz_z, off + P, 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
     return fail(NACHO_ERR_CUDA, "nnz_Z copy");
   return NACHO_SUCCESS;
+}
+
+/* ------------------------------------------------------------------ third-order CSF (csf.cuh) */
+namespace {
+nacho_status check_tensors(const nacho_tensor3* ops, int32_t k, Csf3Args& a) {
+  if (!ops) return fail(NACHO_ERR_INVALID_ARG, "null operand array");
+  if (k < 1 || k > 4) return fail(NACHO_ERR_INVALID_ARG, "k = %d outside [1, 4] (CSF)", k);
+  for (int o = 0; o < k; ++o) {
+    const nacho_tensor3& T = ops[o];
+    if (T.n0 < 0 || T.n1 < 0 || T.n2 < 0 || T.nnz < 0 || T.n_slices < 0 || T.n_fibers < 0)
+      return fail(NACHO_ERR_SHAPE, "tensor %d: negative size", o);
+    if (T.n0 > INT32_MAX || T.n1 > INT32_MAX || T.n2 > INT32_MAX)
+      return fail(NACHO_ERR_OVERFLOW, "tensor %d: a dimension > INT32_MAX", o);
+    if (T.n0 != ops[0].n0 || T.n1 != ops[0].n1 || T.n2 != ops[0].n2 || T.dtype != ops[0].dtype)
+      return fail(NACHO_ERR_SHAPE, "tensor %d disagrees with tensor 0 in shape/dtype", o);
+    if (T.dtype != NACHO_F32 && T.dtype != NACHO_F64) return fail(NACHO_ERR_INVALID_ARG, "tensor %d: dtype", o);
+    if (!T.pos1 || !T.pos2) return fail(NACHO_ERR_INVALID_ARG, "tensor %d: null pos1 / pos2", o);
+    if ((T.n_slices > 0 && !T.crd0) || (T.n_fibers > 0 && !T.crd1) || (T.nnz > 0 && (!T.crd2 || !T.val)))
+      return fail(NACHO_ERR_INVALID_ARG, "tensor %d: null crd / val", o);
+    Csf3View& v = a.op[o];
+    v.n0 = T.n0; v.n1 = T.n1; v.n2 = T.n2; v.nnz = T.nnz; v.ns = T.n_slices; v.nf = T.n_fibers;
+    v.crd0 = T.crd0; v.pos1 = T.pos1; v.crd1 = T.crd1; v.pos2 = T.pos2; v.crd2 = T.crd2; v.val = T.val;
+  }
+  a.k = k;
+  a.n0 = ops[0].n0;
+  return NACHO_SUCCESS;
+}
+}  // namespace
+
+nacho_status nacho_partition_csf(const nacho_tensor3* ops, int32_t k, int32_t P, nacho_parts* out, void* stream) {
+  Csf3Args a;
+  NACHO_TRY(check_tensors(ops, k, a));
+  if (P < 1) return fail(NACHO_ERR_INVALID_ARG, "P = %d < 1", P);
+  NACHO_TRY(check_parts(out, k));
+  if (out->P != P) return fail(NACHO_ERR_INVALID_ARG, "parts.P = %d != P = %d", out->P, P);
+  int64_t qstar = 0;
+  for (int o = 0; o < k; ++o) qstar += ops[o].nnz;
+  out->max_work = (qstar + P - 1) / P + (k - 1);
+  const unsigned g = (unsigned)((P + 1 + 3) / 4);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const PartsArg pa = parts_arg(out);
+  if (k <= 2) csf_partition_kernel<2><<<g, 128, 0, st>>>(a, pa, qstar);
+  else csf_partition_kernel<4><<<g, 128, 0, st>>>(a, pa, qstar);
+  return launched("csf_partition_kernel");
+}
+
+size_t nacho_csf_spadd_k_workspace_size(const nacho_tensor3* ops, int32_t k, int32_t P) {
+  (void)ops; (void)k;
+  const size_t Pe = P > 0 ? P : 1;
+  return 2 * align_up(3 * (Pe + 1) * 8);
+}
+
+nacho_status nacho_csf_spadd_k(const nacho_tensor3* ops, int32_t k, const nacho_parts* parts, int64_t* counts,
+                               int32_t* z_crd0, int64_t* z_pos1, int32_t* z_crd1, int64_t* z_pos2, int32_t* z_crd2,
+                               void* z_val, void* ws, size_t ws_bytes, void* stream) {
+  Csf3Args a;
+  NACHO_TRY(check_tensors(ops, k, a));
+  NACHO_TRY(check_parts(parts, k));
+  if (!counts || !z_pos1 || !z_pos2) return fail(NACHO_ERR_INVALID_ARG, "null output");
+  int64_t qstar = 0;
+  for (int o = 0; o < k; ++o) qstar += ops[o].nnz;
+  if (qstar > 0 && (!z_crd0 || !z_crd1 || !z_crd2 || !z_val)) return fail(NACHO_ERR_INVALID_ARG, "null z_crd / z_val");
+  const int64_t P = parts->P;
+  const size_t need = nacho_csf_spadd_k_workspace_size(ops, k, parts->P);
+  if (!ws || ws_bytes < need) return fail(NACHO_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t* cnt = static_cast<int64_t*>(ws);
+  int64_t* off = reinterpret_cast<int64_t*>(static_cast<char*>(ws) + align_up(3 * (P + 1) * 8));
+  const PartsArg pa = parts_arg(parts);
+  const unsigned g = (unsigned)((P + 127) / 128);
+  const bool f64 = ops[0].dtype == NACHO_F64;
+  if (f64) csf_spadd_kernel<double, 0><<<g, 128, 0, st>>>(a, pa, cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  else csf_spadd_kernel<float, 0><<<g, 128, 0, st>>>(a, pa, cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  NACHO_TRY(launched("csf_spadd_kernel<0>"));
+  for (int l = 0; l < 3; ++l) {
+    rec_scan_kernel<1024><<<1, 1024, 0, st>>>(cnt + l * (P + 1), nullptr, P, off + l * (P + 1));
+    NACHO_TRY(launched("rec_scan_kernel"));
+  }
+  if (f64)
+    csf_spadd_kernel<double, 1><<<g, 128, 0, st>>>(a, pa, nullptr, off, z_crd0, z_pos1, z_crd1, z_pos2, z_crd2,
+                                                    static_cast<double*>(z_val));
+  else
+    csf_spadd_kernel<float, 1><<<g, 128, 0, st>>>(a, pa, nullptr, off, z_crd0, z_pos1, z_crd1, z_pos2, z_crd2,
+                                                   static_cast<float*>(z_val));
+  NACHO_TRY(launched("csf_spadd_kernel<1>"));
+  csf_counts_kernel<<<1, 32, 0, st>>>(off, P, counts);
+  return launched("csf_counts_kernel");
 }
 
 /* ------------------------------------------------------------------ multi-GPU (dist.cuh) */
