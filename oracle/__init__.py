@@ -78,6 +78,13 @@ def lib():
         L.oracle_csf_partition_rank.argtypes = [ctypes.c_int32, vp, ctypes.c_int32, vp]
         L.oracle_csf_spadd_k.argtypes = [ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, vp]
         L.oracle_csf_spadd_k.restype = i64
+        L.oracle_spgemm_work.argtypes = [vp, vp, vp]
+        L.oracle_spgemm_work.restype = i64
+        L.oracle_esc_partition.argtypes = [vp, vp, ctypes.c_int32, vp]
+        L.oracle_spgemm.argtypes = [vp, vp, vp, vp, vp, i64]
+        L.oracle_spgemm.restype = i64
+        L.oracle_sssmm.argtypes = [vp, vp, vp, vp, vp, vp, i64]
+        L.oracle_sssmm.restype = i64
     return _lib
 
 
@@ -392,3 +399,51 @@ def csf_spadd_k(ops):
     ns, nf, ne = (int(x) for x in counts)
     return z[0][:ns], z[1][:ns + 1], z[2][:nf], z[3][:nf + 1], z[4][:ne], z[5][:ne]
 
+
+
+# ------------------------------------------------------------------ ESC scatter kernels
+def spgemm_work(A, B) -> np.ndarray:
+    """W[q] = sum_{q' < q} nnz(B_{A.crd[q']}) for q in [0, nnz(A)] (Listing 6's broadcast-scaled cost)."""
+    arr, keep = _matrices([A, B])
+    W = np.zeros(A.crd.shape[0] + 1, np.int64)
+    if lib().oracle_spgemm_work(ctypes.byref(arr[0]), ctypes.byref(arr[1]), _p(W)) < 0:
+        raise ValueError("oracle_spgemm_work: CSR x CSR with A.ncols == B.nrows")
+    return W
+
+
+def esc_partition(A, B, P) -> Parts:
+    """Boundaries of the expansion: b_p = location of product number Q_p (pos = (A position, B position))."""
+    arr, keep = _matrices([A, B])
+    out = Parts(P, 2)
+    s = out.c()
+    if lib().oracle_esc_partition(ctypes.byref(arr[0]), ctypes.byref(arr[1]), P, ctypes.byref(s)) != 0:
+        raise ValueError("oracle_esc_partition failed")
+    return out
+
+
+def spgemm(A, B):
+    """(c_pos, c_crd, c_val) of C = A B: structural product, left fold over k ascending."""
+    arr, keep = _matrices([A, B])
+    W = spgemm_work(A, B)
+    cap = max(int(W[-1]), 1)
+    c_pos = np.zeros(A.nrows + 1, np.int64)
+    c_crd = np.zeros(cap, np.int32)
+    c_val = np.zeros(cap, dtype=A.val.dtype)
+    n = lib().oracle_spgemm(ctypes.byref(arr[0]), ctypes.byref(arr[1]), _p(c_pos), _p(c_crd), _p(c_val), cap)
+    if n < 0:
+        raise ValueError("oracle_spgemm failed")
+    return c_pos, c_crd[:n].copy(), c_val[:n].copy()
+
+
+def sssmm(S, A, B):
+    """(z_pos, z_crd, z_val) of Z = S (.) (A B): Z_ij = S_ij * C_ij on the coordinates S and C both store."""
+    arr, keep = _matrices([S, A, B])
+    cap = max(int(S.crd.shape[0]), 1)
+    z_pos = np.zeros(S.nrows + 1, np.int64)
+    z_crd = np.zeros(cap, np.int32)
+    z_val = np.zeros(cap, dtype=S.val.dtype)
+    n = lib().oracle_sssmm(ctypes.byref(arr[0]), ctypes.byref(arr[1]), ctypes.byref(arr[2]), _p(z_pos), _p(z_crd),
+                           _p(z_val), cap)
+    if n < 0:
+        raise ValueError("oracle_sssmm failed")
+    return z_pos, z_crd[:n].copy(), z_val[:n].copy()

@@ -876,3 +876,144 @@ overflow:
     return -1;
 }
 
+
+/* ---------------------------------------------------------------- ESC scatter kernels (SpGEMM, SSSMM) */
+/* Appends versus scatters: a kernel that scatters into a sparse output (SpGEMM
+ * C_ij = sum_k A_ik B_kj over the loop order i -> k -> j) is run as expand-sort-contract (ESC):
+ * the expansion T materialises every product A_ik * B_kj with its coordinate (i, j) -- rows i
+ * ascending, A positions q ascending within a row, B positions ascending within row k of B --, a
+ * sort by (i, j) turns the reduction into a segmented reduction, and the contraction folds every
+ * run of equal coordinates.  The load balancing applies to the expansion only. */
+
+/* The cost of the expansion, the broadcast-scaled cost of Listing 6:
+ * A's entry q at (i, k) is coiterated with the whole row k of B (B's j level is not indexed by A),
+ * so it costs nnz(B_k).  W[q] = sum_{q' < q} nnz(B_{A.crd[q']}) for q in [0, nnz(A)]; returns
+ * Q* = W[nnz(A)] (the number of products), or -1 if the shapes disagree. */
+int64_t oracle_spgemm_work(const or_matrix *A, const or_matrix *B, int64_t *W) {
+    if (A->format != OR_CSR || B->format != OR_CSR || A->ncols != B->nrows) return -1;
+    int64_t w = 0;
+    for (int64_t q = 0; q < A->nnz; q++) {
+        W[q] = w;
+        const int64_t k = A->crd[q];
+        w += B->pos[k + 1] - B->pos[k];
+    }
+    W[A->nnz] = w;
+    return w;
+}
+
+/* Partition of the expansion by its definition (Q_p of P:1089-1093 over the cost W): b_p locates
+ * product number Q_p of T -- row[p] = its row i, pos[2p] = the A position q that produces it,
+ * pos[2p+1] = its B position, col[p] = its column j, row_pos[p] = row[p] (CSR).  A query at or past
+ * Q* gives the end (nrows, nnz(A), nnz(B), col 0).  k = 2 in the record.  Returns 0, or 1 on a bad
+ * argument. */
+int oracle_esc_partition(const or_matrix *A, const or_matrix *B, int32_t P, or_parts *out) {
+    if (P < 1 || A->format != OR_CSR || B->format != OR_CSR || A->ncols != B->nrows) return 1;
+    int64_t *W = (int64_t *)malloc(sizeof(int64_t) * (size_t)(A->nnz + 1));
+    const int64_t qstar = oracle_spgemm_work(A, B, W);
+    oracle_queries(qstar, P, out->query);
+    int64_t q = 0, i = 0;
+    for (int32_t p = 0; p <= P; p++) {
+        const int64_t Q = out->query[p];
+        if (Q >= qstar) {
+            out->row[p] = A->nrows; out->row_pos[p] = A->nrows; out->col[p] = 0;
+            out->pos[2 * (int64_t)p] = A->nnz; out->pos[2 * (int64_t)p + 1] = B->nnz;
+            continue;
+        }
+        while (W[q + 1] <= Q) q++;               /* the entry with W[q] <= Q < W[q + 1] */
+        while (A->pos[i + 1] <= q) i++;          /* its row */
+        const int64_t bp = B->pos[A->crd[q]] + (Q - W[q]);
+        out->row[p] = i; out->row_pos[p] = i; out->col[p] = B->crd[bp];
+        out->pos[2 * (int64_t)p] = q; out->pos[2 * (int64_t)p + 1] = bp;
+    }
+    free(W);
+    return 0;
+}
+
+static int cmp_i32(const void *a, const void *b) {
+    const int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* C = A B, CSR x CSR -> CSR, with ESC's result: C stores (i, j) iff some k has A_ik and B_kj stored
+ * (structurally, whatever the sum); the value is the left fold over k ascending (the order a stable
+ * sort of T by (i, j) keeps) of the products A_ik * B_kj, each rounded in the value type, starting
+ * from the first product (reading R22).  Row by row with a dense accumulator (Gustavson's order,
+ * the same fold).  Returns nnz(C), or -1 (shape / capacity). */
+int64_t oracle_spgemm(const or_matrix *A, const or_matrix *B, int64_t *c_pos, int32_t *c_crd, void *c_val,
+                      int64_t cap) {
+    if (A->format != OR_CSR || B->format != OR_CSR || A->ncols != B->nrows) return -1;
+    const int f64 = A->dtype == OR_F64;
+    const int64_t N = B->ncols;
+    int64_t *stamp = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N > 0 ? N : 1));
+    double *accd = (double *)malloc(sizeof(double) * (size_t)(N > 0 ? N : 1));
+    float *accf = (float *)malloc(sizeof(float) * (size_t)(N > 0 ? N : 1));
+    int32_t *cols = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N > 0 ? N : 1));
+    for (int64_t j = 0; j < N; j++) stamp[j] = -1;
+    int64_t nz = 0;
+    c_pos[0] = 0;
+    for (int64_t i = 0; i < A->nrows; i++) {
+        int64_t nc = 0;
+        for (int64_t q = A->pos[i]; q < A->pos[i + 1]; q++) {
+            const int64_t k = A->crd[q];
+            for (int64_t r = B->pos[k]; r < B->pos[k + 1]; r++) {
+                const int64_t j = B->crd[r];
+                const int first = stamp[j] != i;
+                if (first) { stamp[j] = i; cols[nc++] = (int32_t)j; }
+                if (f64) {
+                    const double t = ((const double *)A->val)[q] * ((const double *)B->val)[r];
+                    accd[j] = first ? t : accd[j] + t;
+                } else {
+                    const float t = ((const float *)A->val)[q] * ((const float *)B->val)[r];
+                    accf[j] = first ? t : accf[j] + t;
+                }
+            }
+        }
+        qsort(cols, (size_t)nc, sizeof(int32_t), cmp_i32);
+        if (nz + nc > cap) { nz = -1; break; }
+        for (int64_t u = 0; u < nc; u++) {
+            const int32_t j = cols[u];
+            c_crd[nz] = j;
+            if (f64) ((double *)c_val)[nz] = accd[j]; else ((float *)c_val)[nz] = accf[j];
+            nz++;
+        }
+        c_pos[i + 1] = nz;
+    }
+    free(stamp); free(accd); free(accf); free(cols);
+    return nz;
+}
+
+/* Sampled SpGEMM (SSSMM): Z = S (.) (A B).  Z stores (i, j) iff S stores it and C = A B
+ * stores it structurally; Z_ij = S_ij * C_ij with C_ij the ESC fold of oracle_spgemm (reading R23:
+ * the sampling restricts the expansion to j in S_i, which leaves the products of every kept (i, j)
+ * and their order unchanged, and the sampled value scales the contracted sum).  Returns nnz(Z) or
+ * -1. */
+int64_t oracle_sssmm(const or_matrix *S, const or_matrix *A, const or_matrix *B, int64_t *z_pos, int32_t *z_crd,
+                     void *z_val, int64_t cap) {
+    if (S->format != OR_CSR || S->nrows != A->nrows || S->ncols != B->ncols || S->dtype != A->dtype) return -1;
+    int64_t cap_c = 0;
+    for (int64_t q = 0; q < A->nnz; q++) cap_c += B->pos[A->crd[q] + 1] - B->pos[A->crd[q]];
+    const int f64 = A->dtype == OR_F64;
+    int64_t *c_pos = (int64_t *)malloc(sizeof(int64_t) * (size_t)(A->nrows + 1));
+    int32_t *c_crd = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cap_c > 0 ? cap_c : 1));
+    void *c_val = malloc((f64 ? 8 : 4) * (size_t)(cap_c > 0 ? cap_c : 1));
+    int64_t nz = oracle_spgemm(A, B, c_pos, c_crd, c_val, cap_c);
+    if (nz < 0) goto out;
+    nz = 0;
+    z_pos[0] = 0;
+    for (int64_t i = 0; i < S->nrows; i++) {
+        int64_t s = S->pos[i], c = c_pos[i];
+        while (s < S->pos[i + 1] && c < c_pos[i + 1]) {
+            if (S->crd[s] < c_crd[c]) { s++; continue; }
+            if (S->crd[s] > c_crd[c]) { c++; continue; }
+            if (nz >= cap) { nz = -1; goto out; }
+            z_crd[nz] = S->crd[s];
+            if (f64) ((double *)z_val)[nz] = ((const double *)S->val)[s] * ((const double *)c_val)[c];
+            else     ((float *)z_val)[nz]  = ((const float *)S->val)[s] * ((const float *)c_val)[c];
+            nz++; s++; c++;
+        }
+        z_pos[i + 1] = nz;
+    }
+out:
+    free(c_pos); free(c_crd); free(c_val);
+    return nz;
+}

@@ -133,6 +133,18 @@ int64_t oracle_csf_spadd_k(int32_t k, const or_tensor3 *ops, int32_t *z_crd0, in
                            int64_t *z_pos2, int32_t *z_crd2, void *z_val, int64_t cap_s, int64_t cap_f, int64_t cap_e,
                            int64_t *counts);
 
+/* ESC scatter kernels: SpGEMM C = A B over i -> k -> j and sampled SpGEMM Z = S (.) (A B).
+ * W[nnz(A)+1]: exclusive prefix of nnz(B_{A.crd[q]}) (Listing 6's broadcast-scaled cost); returns Q*. */
+int64_t oracle_spgemm_work(const or_matrix *A, const or_matrix *B, int64_t *W);
+/* b_p = location of product number Q_p of the expansion (k = 2 record: pos = A position, B position). */
+int     oracle_esc_partition(const or_matrix *A, const or_matrix *B, int32_t P, or_parts *out);
+/* C = A B (CSR): structural product, left fold over k ascending in the value type; nnz(C) or -1. */
+int64_t oracle_spgemm(const or_matrix *A, const or_matrix *B, int64_t *c_pos, int32_t *c_crd, void *c_val,
+                      int64_t cap);
+/* Z = S (.) (A B): Z_ij = S_ij * C_ij on the stored coordinates of both; nnz(Z) or -1. */
+int64_t oracle_sssmm(const or_matrix *S, const or_matrix *A, const or_matrix *B, int64_t *z_pos, int32_t *z_crd,
+                     void *z_val, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif
