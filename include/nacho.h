@@ -294,6 +294,53 @@ nacho_status nacho_csf_spadd_k(const nacho_tensor3* ops, int32_t k, const nacho_
                                void* z_val, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------------------------
+ * ESC scatter kernels: a kernel that scatters into a sparse output runs as
+ * expand - sort - contract, with the load balancing applied to the expansion only
+ * (P:2073-2074).  SpGEMM C = A B over i -> k -> j; sampled SpGEMM Z = S (.) (A B)
+ * (SSSMM).  A, B, S CSR of one dtype; A.ncols == B.nrows; S is A.nrows x B.ncols.
+ * ------------------------------------------------------------------------------------------------ */
+
+/* nacho_spgemm_work -- the expansion's cost, Listing 6's broadcast-scaled cost (P:1714-1727,
+ * P:1742-1749): W[q] = sum_{q' < q} nnz(B_{A.crd[q']}) for q in [0, nnz(A)] (device int64[nnz(A)+1]);
+ * W[nnz(A)] = Q*, the number of products (the caller reads it to size the expansion). */
+size_t nacho_spgemm_work_workspace_size(const nacho_matrix* A);
+nacho_status nacho_spgemm_work(const nacho_matrix* A, const nacho_matrix* B, int64_t* W, void* ws, size_t ws_bytes,
+                               void* stream);
+/* P for about 8192 products per partition. */
+int32_t nacho_esc_auto_partitions(int64_t qstar);
+
+/* nacho_partition_esc -- Alg. 1 over i -> k -> j with the cost W: Q_p = floor(p Q* / P)
+ * (P:1089-1093); b_p locates product number Q_p of the expansion (rows ascending, A positions, B
+ * positions): row[p] = row_pos[p] = its row i, pos[2p] = the A position q producing it, pos[2p+1] = its
+ * B position, col[p] = its column j.  A query at or past Q* gives (nrows, nnz(A), nnz(B), col 0).  out
+ * must have k == 2 and P == P; max_work is set to floor(Q* / P) + 1. */
+nacho_status nacho_partition_esc(const nacho_matrix* A, const nacho_matrix* B, const int64_t* W, int64_t qstar,
+                                 int32_t P, nacho_parts* out, void* stream);
+
+/* nacho_spgemm_esc -- C = A B: expand (one CTA per partition writes the products [Q_p, Q_{p+1}) at
+ * their expansion index: key (i, j), value A_ik * B_kj), stable radix sort by (i, j), contract (every
+ * run of one (i, j) folded left to right, i.e. k ascending -- reading R22).  C stores (i, j) iff some
+ * product has that coordinate.  c_pos[A.nrows+1], c_crd / c_val capacity >= Q*; *nnz_c (device int64)
+ * receives nnz(C).  The workspace holds the expansion twice (sort buffers) and the run indices. */
+size_t nacho_spgemm_esc_workspace_size(const nacho_matrix* A, const nacho_matrix* B, int64_t qstar);
+nacho_status nacho_spgemm_esc(const nacho_matrix* A, const nacho_matrix* B, const int64_t* W, const nacho_parts* parts,
+                              int64_t qstar, int64_t* c_pos, int32_t* c_crd, void* c_val, int64_t* nnz_c, void* ws,
+                              size_t ws_bytes, void* stream);
+
+/* nacho_sssmm_esc_count / nacho_sssmm_esc -- Z = S (.) (A B) (reading R23: Z_ij = S_ij * C_ij on the
+ * coordinates S and C both store).  The expansion over the same W / partition keeps the products whose
+ * j is stored in S_i: count per partition -> part_off (device int64[P+1], exclusive prefix; part_off[P]
+ * = kept products, which the caller reads) -> fill in expansion order -> sort -> contract.  Z
+ * capacity >= part_off[P]. */
+size_t nacho_sssmm_count_workspace_size(int32_t P);
+nacho_status nacho_sssmm_esc_count(const nacho_matrix* S, const nacho_matrix* A, const nacho_matrix* B, const int64_t* W,
+                                   const nacho_parts* parts, int64_t* part_off, void* ws, size_t ws_bytes, void* stream);
+size_t nacho_sssmm_esc_workspace_size(const nacho_matrix* A, const nacho_matrix* B, int64_t n_kept);
+nacho_status nacho_sssmm_esc(const nacho_matrix* S, const nacho_matrix* A, const nacho_matrix* B, const int64_t* W,
+                             const nacho_parts* parts, const int64_t* part_off, int64_t n_kept, int64_t* z_pos,
+                             int32_t* z_crd, void* z_val, int64_t* nnz_z, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------------------------
  * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.
  * Synchronous on `stream` (it reads one flag back).  Returns NACHO_ERR_FORMAT on a violation. */
 nacho_status nacho_validate(const nacho_matrix* A, void* stream);

@@ -94,6 +94,22 @@ def _load():
     L.nacho_csf_spadd_k_workspace_size.argtypes = [vp, i32, i32]
     L.nacho_csf_spadd_k_workspace_size.restype = sz
     L.nacho_csf_spadd_k.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    # ESC scatter kernels (esc.cu)
+    L.nacho_spgemm_work_workspace_size.argtypes = [vp]
+    L.nacho_spgemm_work_workspace_size.restype = sz
+    L.nacho_spgemm_work.argtypes = [vp, vp, vp, vp, sz, vp]
+    L.nacho_esc_auto_partitions.argtypes = [i64]
+    L.nacho_esc_auto_partitions.restype = i32
+    L.nacho_partition_esc.argtypes = [vp, vp, vp, i64, i32, vp, vp]
+    L.nacho_spgemm_esc_workspace_size.argtypes = [vp, vp, i64]
+    L.nacho_spgemm_esc_workspace_size.restype = sz
+    L.nacho_spgemm_esc.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_sssmm_count_workspace_size.argtypes = [i32]
+    L.nacho_sssmm_count_workspace_size.restype = sz
+    L.nacho_sssmm_esc_count.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_sssmm_esc_workspace_size.argtypes = [vp, vp, i64]
+    L.nacho_sssmm_esc_workspace_size.restype = sz
+    L.nacho_sssmm_esc.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]
     # multi-GPU (dist.cuh)
     L.nacho_dist_unique_id_size.restype = sz
     L.nacho_dist_unique_id.argtypes = [vp]
@@ -122,6 +138,10 @@ EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", 
            "nacho_dcsr_hadamard_workspace_size", "nacho_dcsr_hadamard", "nacho_dcsr_spadd_k_workspace_size",
            "nacho_dcsr_spadd_k", "nacho_mixed_spadd_k_workspace_size", "nacho_mixed_spadd_k",
            "nacho_partition_csf", "nacho_csf_spadd_k_workspace_size", "nacho_csf_spadd_k",
+           "nacho_spgemm_work_workspace_size", "nacho_spgemm_work", "nacho_esc_auto_partitions",
+           "nacho_partition_esc", "nacho_spgemm_esc_workspace_size", "nacho_spgemm_esc",
+           "nacho_sssmm_count_workspace_size", "nacho_sssmm_esc_count", "nacho_sssmm_esc_workspace_size",
+           "nacho_sssmm_esc",
            "nacho_dist_unique_id_size", "nacho_dist_unique_id", "nacho_dist_init",
            "nacho_dist_destroy", "nacho_dist_broadcast", "nacho_device_cuts", "nacho_shard_rows", "nacho_dist_seam",
            "nacho_dist_spmv_workspace_size", "nacho_dist_spmv", "nacho_dist_spadd_workspace_size",
@@ -509,6 +529,94 @@ def csf_spadd_k(ops, parts: Parts, stream=None):
                                  _stream(stream)))
     ns, nf, ne = (int(v) for v in counts.cpu().tolist())
     return z[0][:ns], z[1][:ns + 1], z[2][:nf], z[3][:nf + 1], z[4][:ne], z[5][:ne]
+
+
+# ------------------------------------------------------------------ ESC scatter kernels (esc.cu)
+def spgemm_work(A, B, W=None, stream=None):
+    """nacho_spgemm_work: W[q] = sum_{q' < q} nnz(B_{A.crd[q']}) (device int64[nnz(A)+1])."""
+    a, b = matrix(A), matrix(B)
+    dev = A.pos.device
+    if W is None:
+        W = torch.empty(A.nnz + 1, dtype=torch.int64, device=dev)
+    need = lib.nacho_spgemm_work_workspace_size(ctypes.byref(a))
+    ws, _ = _workspace(need, dev)
+    _check(lib.nacho_spgemm_work(ctypes.byref(a), ctypes.byref(b), _ptr(W), _ptr(ws), need, _stream(stream)))
+    return W
+
+
+def partition_esc(A, B, W, qstar: int, P: int, out: Parts = None, stream=None) -> Parts:
+    """nacho_partition_esc: b_p locates product number Q_p of the expansion (k = 2 record)."""
+    a, b = matrix(A), matrix(B)
+    out = out or Parts(P, 2, A.pos.device)
+    pc = out.c()
+    _check(lib.nacho_partition_esc(ctypes.byref(a), ctypes.byref(b), _ptr(W), qstar, P, ctypes.byref(pc),
+                                   _stream(stream)))
+    out.max_work = pc.max_work
+    return out
+
+
+def esc_auto_partitions(qstar: int) -> int:
+    return lib.nacho_esc_auto_partitions(qstar)
+
+
+def spgemm_esc(A, B, W, parts: Parts, qstar: int, c_pos=None, c_crd=None, c_val=None, nnz_c=None, ws=None,
+               stream=None):
+    """nacho_spgemm_esc: C = A B by expand - sort - contract.  Returns (c_pos, c_crd, c_val, nnz_c) with
+    c_crd / c_val of capacity Q* (nnz_c a device int64[1]; the caller trims)."""
+    a, b = matrix(A), matrix(B)
+    dev = A.pos.device
+    if c_pos is None:
+        c_pos = torch.empty(A.nrows + 1, dtype=torch.int64, device=dev)
+        c_crd = torch.empty(max(qstar, 1), dtype=torch.int32, device=dev)
+        c_val = torch.empty(max(qstar, 1), dtype=A.val.dtype, device=dev)
+        nnz_c = torch.empty(1, dtype=torch.int64, device=dev)
+    need = lib.nacho_spgemm_esc_workspace_size(ctypes.byref(a), ctypes.byref(b), qstar)
+    if ws is None or ws.numel() < need:
+        ws, _ = _workspace(need, dev)
+    pc = parts.c()
+    _check(lib.nacho_spgemm_esc(ctypes.byref(a), ctypes.byref(b), _ptr(W), ctypes.byref(pc), qstar, _ptr(c_pos),
+                                _ptr(c_crd), _ptr(c_val), _ptr(nnz_c), _ptr(ws), need, _stream(stream)))
+    return c_pos, c_crd, c_val, nnz_c
+
+
+def spgemm(A, B, P: int = None, stream=None):
+    """C = A B (ESC): work -> host reads Q* -> partition -> expand / sort / contract -> trimmed C."""
+    W = spgemm_work(A, B, stream=stream)
+    qstar = int(W[-1].item())
+    P = P or esc_auto_partitions(qstar)
+    parts = partition_esc(A, B, W, qstar, P, stream=stream)
+    c_pos, c_crd, c_val, nnz_c = spgemm_esc(A, B, W, parts, qstar, stream=stream)
+    n = int(nnz_c.item())
+    return c_pos, c_crd[:n], c_val[:n]
+
+
+def sssmm(S, A, B, P: int = None, stream=None):
+    """Z = S (.) (A B) (ESC over the sampled expansion): work -> partition -> count -> host reads the kept
+    count -> fill / sort / contract -> trimmed Z."""
+    s, a, b = matrix(S), matrix(A), matrix(B)
+    dev = A.pos.device
+    W = spgemm_work(A, B, stream=stream)
+    qstar = int(W[-1].item())
+    P = P or esc_auto_partitions(qstar)
+    parts = partition_esc(A, B, W, qstar, P, stream=stream)
+    part_off = torch.empty(P + 1, dtype=torch.int64, device=dev)
+    need = lib.nacho_sssmm_count_workspace_size(P)
+    ws, _ = _workspace(need, dev)
+    pc = parts.c()
+    _check(lib.nacho_sssmm_esc_count(ctypes.byref(s), ctypes.byref(a), ctypes.byref(b), _ptr(W), ctypes.byref(pc),
+                                     _ptr(part_off), _ptr(ws), need, _stream(stream)))
+    n_kept = int(part_off[-1].item())
+    z_pos = torch.empty(A.nrows + 1, dtype=torch.int64, device=dev)
+    z_crd = torch.empty(max(n_kept, 1), dtype=torch.int32, device=dev)
+    z_val = torch.empty(max(n_kept, 1), dtype=A.val.dtype, device=dev)
+    nnz_z = torch.empty(1, dtype=torch.int64, device=dev)
+    need = lib.nacho_sssmm_esc_workspace_size(ctypes.byref(a), ctypes.byref(b), n_kept)
+    ws, _ = _workspace(need, dev)
+    _check(lib.nacho_sssmm_esc(ctypes.byref(s), ctypes.byref(a), ctypes.byref(b), _ptr(W), ctypes.byref(pc),
+                               _ptr(part_off), n_kept, _ptr(z_pos), _ptr(z_crd), _ptr(z_val), _ptr(nnz_z), _ptr(ws),
+                               need, _stream(stream)))
+    n = int(nnz_z.item())
+    return z_pos, z_crd[:n], z_val[:n]
 
 
 # ------------------------------------------------------------------ multi-GPU (include/nacho.h, dist.cuh)

@@ -31,7 +31,8 @@ def build_nacho(force=False, verbose=False):
     if force or _newer(out, srcs):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
                f"--split-compile={max(1, min(16, os.cpu_count() or 1))}",   # device code optimised in parallel
-               "-I", os.path.join(ROOT, "include"), "-o", out, os.path.join(HERE, "csrc", "api.cu")]
+               "-I", os.path.join(ROOT, "include"), "-o", out, os.path.join(HERE, "csrc", "api.cu"),
+               os.path.join(HERE, "csrc", "esc.cu")]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)

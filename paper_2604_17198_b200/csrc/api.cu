@@ -625,6 +625,10 @@ int spadd_impl() {
 
 }  // namespace
 
+// status plumbing for the other translation units of the library (esc.cu)
+nacho_status nacho_internal_fail(nacho_status s, const char* msg) { return fail(s, "%s", msg); }
+nacho_status nacho_internal_launched(const char* what) { return launched(what); }
+
 extern "C" {
 
 /* ------------------------------------------------------------------ k-way intersection (spadd7, OP) */
