@@ -669,6 +669,73 @@ def bench_spmm(N, W, torch, scale, K, Wu, timer):
                 wl=wl)
 
 
+def bench_esc(N, W, torch, scale, K, Wu, timer, sampled=False):
+    """ESC scatter kernels on C2's operands: SpGEMM C = A B (A, B = C2's first two
+    operands), or with sampled=True the sampled SpGEMM Z = S (.) (A B) with S = C2's third operand.
+    One step = work W (Listing 6's cost) + partition of the expansion + expand / sort / contract
+    (sampled: + the count pass).  Work unit: products of the expansion (Q*).  Q* and the sampled count
+    are read once at setup (they size the buffers), not inside the timed steps."""
+    wl = W.build("c2", scale, device="cuda")
+    A, B, S = wl.ops
+    M = A.nrows
+    Wd = N.spgemm_work(A, B)
+    qstar = int(Wd[-1].item())
+    P = N.esc_auto_partitions(qstar)
+    parts = N.partition_esc(A, B, Wd, qstar, P)
+    sa, aa, ba = N.matrix(S), N.matrix(A), N.matrix(B)
+    import ctypes
+    if sampled:
+        part_off = torch.empty(P + 1, dtype=torch.int64, device="cuda")
+        cws = torch.empty(max(1, N.lib.nacho_sssmm_count_workspace_size(P)), dtype=torch.uint8, device="cuda")
+        pc = parts.c()
+        N._check(N.lib.nacho_sssmm_esc_count(ctypes.byref(sa), ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd),
+                                             ctypes.byref(pc), N._ptr(part_off), N._ptr(cws), cws.numel(), None))
+        n = int(part_off[-1].item())
+    else:
+        n = qstar
+    need = N.lib.nacho_spgemm_esc_workspace_size(ctypes.byref(aa), ctypes.byref(ba), n)
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    wws = torch.empty(max(1, N.lib.nacho_spgemm_work_workspace_size(ctypes.byref(aa))), dtype=torch.uint8, device="cuda")
+    c_pos = torch.empty(M + 1, dtype=torch.int64, device="cuda")
+    c_crd = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    c_val = torch.empty(max(n, 1), dtype=torch.float32, device="cuda")
+    nnz_c = torch.empty(1, dtype=torch.int64, device="cuda")
+
+    def step(timed=False):
+        m = [ev(torch)] if timed else None
+        N._check(N.lib.nacho_spgemm_work(ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd), N._ptr(wws), wws.numel(), None))
+        if timed:
+            m.append(ev(torch))
+        pc = parts.c()
+        N._check(N.lib.nacho_partition_esc(ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd), qstar, P, ctypes.byref(pc),
+                                           None))
+        if timed:
+            m.append(ev(torch))
+        if sampled:
+            N._check(N.lib.nacho_sssmm_esc_count(ctypes.byref(sa), ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd),
+                                                 ctypes.byref(pc), N._ptr(part_off), N._ptr(cws), cws.numel(), None))
+            if timed:
+                m.append(ev(torch))
+            N._check(N.lib.nacho_sssmm_esc(ctypes.byref(sa), ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd),
+                                           ctypes.byref(pc), N._ptr(part_off), n, N._ptr(c_pos), N._ptr(c_crd),
+                                           N._ptr(c_val), N._ptr(nnz_c), N._ptr(ws), need, None))
+        else:
+            N._check(N.lib.nacho_spgemm_esc(ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd), ctypes.byref(pc), qstar,
+                                            N._ptr(c_pos), N._ptr(c_crd), N._ptr(c_val), N._ptr(nnz_c), N._ptr(ws),
+                                            need, None))
+        if timed:
+            m.append(ev(torch))
+        return m
+    secs = ["work", "partition"] + (["count", "fill+sort+contract"] if sampled else ["expand+sort+contract"])
+    times, sec = timer.run(step, K, Wu, secs)
+    nnz_out = int(nnz_c.item())
+    io = A.nnz * 8 + (M + 1) * 8 + B.nnz * 8 + (B.nrows + 1) * 8 + nnz_out * 8 + (M + 1) * 8
+    esc = io + 24 * n + (S.nnz * 8 + (M + 1) * 8 if sampled else 0)   # + the expansion written and read once
+    return dict(work=qstar, times=times, sec=sec, algo_step=esc, kernel_bytes={secs[-1]: esc, "work": A.nnz * 12,
+                "partition": (P + 1) * 44, "count": A.nnz * 8}, P=P, dtype="f32", wl=wl, n_products=qstar,
+                n_kept=n, nnz_out=nnz_out)
+
+
 def summarize(r, peak, world=1):
     ms = statistics.mean(r["times"])
     dom = max(r["sec"], key=lambda s: statistics.mean(r["sec"][s]))
@@ -915,6 +982,8 @@ def main():
                          ("c4_spmm_f32_nb64", lambda: bench_spmm(N, W, torch, args.scale, 5, 2, timer)),
                          ("c2_hadamard3_and_inner", lambda: bench_intersection(N, W, torch, args.scale, 10, 3, timer)),
                          ("c3_dcsr_hadamard_recursive", lambda: bench_recursive(N, W, torch, args.scale, 5, 2, timer)),
+                         ("c2ops_spgemm_esc", lambda: bench_esc(N, W, torch, args.scale, 5, 2, timer)),
+                         ("c2ops_sssmm_esc", lambda: bench_esc(N, W, torch, args.scale, 5, 2, timer, sampled=True)),
                          ("c1_spmv_csr_f64_P8", lambda: bench_spmv(N, W, torch, "c1", 1.0, 20, 3, timer))]:
             try:
                 rr = fn()
@@ -926,6 +995,9 @@ def main():
                               "step_hbm_frac": s["step_hbm_frac"], "dominant": d,
                               "dominant_hbm_frac": ach / peak, "dominant_frac_nominal_8tbs": ach / NOMINAL_HBM_GBS, "sections_ms": s["sections_ms"], "P": s["P"],
                               "traffic": traffic_table().get(f"{name.split('_')[0]}:{d}")}
+                if "n_products" in rr:   # ESC lines: gnnz_s counts products of the expansion
+                    kern[name].update(unit="G products/s", products=rr["n_products"], kept=rr["n_kept"],
+                                      nnz_out=rr["nnz_out"])
                 del rr
             except Exception as e:  # report, never hide
                 kern[name] = {"error": repr(e)[:300]}

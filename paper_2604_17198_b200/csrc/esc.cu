@@ -103,9 +103,19 @@ struct EscExpandArgs {
   V* val;
 };
 
+// One CTA per partition, in chunks of kEscChunk products: thread t walks products
+// [c0 + 8t, c0 + 8t + 8) sequentially -- one search for the first product's A entry q and row i,
+// then q / i advance as the product index passes W[q + 1] / A.pos[i + 1] (zero-cost entries and empty
+// rows are stepped over) and B's row k is read in order -- and the chunk is staged in shared memory
+// so that the expansion is written with coalesced stores.
+constexpr int kEscVT = 8;
+constexpr int kEscChunk = kEscThreads * kEscVT;
+
 template <typename V, int MODE>
 __global__ void __launch_bounds__(kEscThreads) esc_expand_kernel(const EscExpandArgs<V> a) {
-  __shared__ int32_t wsum[kEscThreads / 32];
+  __shared__ unsigned long long skey[MODE == kEscCount ? 1 : kEscChunk];
+  __shared__ V sval[MODE == kEscCount ? 1 : kEscChunk];
+  __shared__ int32_t wsum[kEscThreads / 32 + 1];
   const EscOps& o = a.o;
   const int64_t p = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -118,50 +128,98 @@ __global__ void __launch_bounds__(kEscThreads) esc_expand_kernel(const EscExpand
   const V* bv = static_cast<const V*>(o.b_val);
   int64_t run = MODE == kEscFill ? a.cnt[p] : 0;   // kept products written so far
   int64_t kept = 0;
-  for (int64_t w0 = Q0; w0 < Q1; w0 += kEscThreads) {
-    const int64_t w = w0 + tid;
-    bool keep = false;
-    int64_t i = 0, q = 0, r = 0;
-    int32_t j = 0;
-    if (w < Q1) {
-      // the A entry producing product w: the largest q in [q0, q1] with W[q] <= w
-      int64_t lo = q0, hi = q1;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (ldg(o.W + mid) <= w) lo = mid; else hi = mid - 1;
+  for (int64_t c0 = Q0; c0 < Q1; c0 += kEscChunk) {
+    const int64_t wb = c0 + (int64_t)tid * kEscVT;
+    const int64_t we = min(wb + kEscVT, Q1);
+    unsigned long long kk[kEscVT];
+    V vv[kEscVT];
+    uint32_t keep = 0;
+    if (wb < we) {
+      // the A entry producing product wb: the largest q in [q0, q1] with W[q] <= wb; its row i
+      int64_t q = q0, hi = q1;
+      while (q < hi) {
+        const int64_t mid = (q + hi + 1) >> 1;
+        if (ldg(o.W + mid) <= wb) q = mid; else hi = mid - 1;
       }
-      q = lo;
-      // its row: the largest i in [x0, x1] with A.pos[i] <= q
-      int64_t rl = x0, rh = x1;
-      while (rl < rh) {
-        const int64_t mid = (rl + rh + 1) >> 1;
-        if (ldg(o.a_pos + mid) <= q) rl = mid; else rh = mid - 1;
+      int64_t i = x0, rh = x1;
+      while (i < rh) {
+        const int64_t mid = (i + rh + 1) >> 1;
+        if (ldg(o.a_pos + mid) <= q) i = mid; else rh = mid - 1;
       }
-      i = rl;
-      const int64_t k = ldg(o.a_crd + q);
-      r = ldg(o.b_pos + k) + (w - ldg(o.W + q));
-      j = ldg(o.b_crd + r);
-      keep = true;
-      if (MODE != kEscAll) {   // sampled: j stored in S_i?
-        int64_t sl = ldg(o.s_pos + i), sh = ldg(o.s_pos + i + 1);
-        while (sl < sh) {
-          const int64_t mid = (sl + sh) >> 1;
-          if (ldg(o.s_crd + mid) < j) sl = mid + 1; else sh = mid;
+      int64_t wq = ldg(o.W + q), wn = ldg(o.W + q + 1);
+      int64_t apn = ldg(o.a_pos + i + 1);
+      int64_t bs = ldg(o.b_pos + ldg(o.a_crd + q));
+      V a_iq = ldg(av + q);
+      int64_t sp = 0, se = 0;   // sampled: cursor in S_i (valid for the current q)
+      bool fresh = true;
+#pragma unroll
+      for (int v = 0; v < kEscVT; ++v) {
+        const int64_t w = wb + v;
+        if (w < we) {
+          if (w >= wn) {   // next A entry with a product (entries without one are stepped over)
+            do {
+              ++q;
+              wq = wn;
+              wn = ldg(o.W + q + 1);
+            } while (w >= wn);
+            while (apn <= q) apn = ldg(o.a_pos + (++i) + 1);
+            bs = ldg(o.b_pos + ldg(o.a_crd + q));
+            a_iq = ldg(av + q);
+            fresh = true;
+          }
+          const int64_t r = bs + (w - wq);
+          const int32_t j = ldg(o.b_crd + r);
+          bool kp = true;
+          if (MODE != kEscAll) {   // sampled: is j stored in S_i?  (j rises along B's row: gallop)
+            if (fresh) {
+              sp = ldg(o.s_pos + i);
+              se = ldg(o.s_pos + i + 1);
+              fresh = false;
+            }
+            int g = 0;
+            while (sp < se && ldg(o.s_crd + sp) < j && g < 4) { ++sp; ++g; }
+            if (sp < se && ldg(o.s_crd + sp) < j) {
+              int64_t lo = sp + 1, h2 = se;
+              while (lo < h2) {
+                const int64_t mid = (lo + h2) >> 1;
+                if (ldg(o.s_crd + mid) < j) lo = mid + 1; else h2 = mid;
+              }
+              sp = lo;
+            }
+            kp = sp < se && ldg(o.s_crd + sp) == j;
+          }
+          if (kp) {
+            keep |= 1u << v;
+            if (MODE != kEscCount) {
+              kk[v] = ((unsigned long long)i << o.jbits) | (unsigned long long)(uint32_t)j;
+              vv[v] = a_iq * ldg(bv + r);
+            }
+          }
         }
-        keep = sl < ldg(o.s_pos + i + 1) && ldg(o.s_crd + sl) == j;
       }
     }
-    if (MODE == kEscAll) {
-      if (keep) {
-        a.key[w] = ((unsigned long long)i << o.jbits) | (unsigned long long)(uint32_t)j;
-        a.val[w] = ldg(av + q) * ldg(bv + r);
+    const int n_chunk = (int)min((int64_t)kEscChunk, Q1 - c0);
+    if (MODE == kEscAll) {   // every product at its expansion index
+#pragma unroll
+      for (int v = 0; v < kEscVT; ++v)
+        if (keep & (1u << v)) { skey[tid * kEscVT + v] = kk[v]; sval[tid * kEscVT + v] = vv[v]; }
+      __syncthreads();
+      for (int u = tid; u < n_chunk; u += kEscThreads) {
+        a.key[c0 + u] = skey[u];
+        a.val[c0 + u] = sval[u];
       }
+      __syncthreads();
       continue;
     }
-    // rank of the kept products of this chunk in expansion order (block exclusive scan of flags)
-    const unsigned bal = __ballot_sync(kFull, keep);
-    const int wrank = __popc(bal & ((1u << lane) - 1u));
-    if (lane == 0) wsum[wid] = __popc(bal);
+    // kept products: rank in expansion order (block exclusive scan of the per-thread counts)
+    const int cnt = __popc(keep);
+    int x = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
     __syncthreads();
     int before = 0, tot = 0;
 #pragma unroll
@@ -170,12 +228,18 @@ __global__ void __launch_bounds__(kEscThreads) esc_expand_kernel(const EscExpand
       before += u < wid ? c : 0;
       tot += c;
     }
-    __syncthreads();
-    if (MODE == kEscFill && keep) {
-      const int64_t z = run + before + wrank;
-      a.key[z] = ((unsigned long long)i << o.jbits) | (unsigned long long)(uint32_t)j;
-      a.val[z] = ldg(av + q) * ldg(bv + r);
+    if (MODE == kEscFill) {
+      int z = before + x - cnt;
+#pragma unroll
+      for (int v = 0; v < kEscVT; ++v)
+        if (keep & (1u << v)) { skey[z] = kk[v]; sval[z] = vv[v]; ++z; }
+      __syncthreads();
+      for (int u = tid; u < tot; u += kEscThreads) {
+        a.key[run + u] = skey[u];
+        a.val[run + u] = sval[u];
+      }
     }
+    __syncthreads();
     run += tot;
     kept += tot;
   }

@@ -139,3 +139,27 @@ def test_c2_fullscale_spadd_all_paths():
     assert np.array_equal(z_pos.cpu().numpy(), rp)
     assert np.array_equal(z_crd.cpu().numpy(), rc)
     assert np.array_equal(z_val.cpu().numpy().view(np.uint32), rv.view(np.uint32))
+
+
+def test_esc_spgemm_bench_scale():
+    """The ESC SpGEMM line of bench.py at its own size (C2's operands A B, ~1e8 products, auto P):
+    W, every boundary and the whole of C bit-exact against the oracle."""
+    wl = W.build("c2", 1.0, device="cuda")
+    A, B = wl.ops[0], wl.ops[1]
+    hA, hB = A.numpy(), B.numpy()
+    Wd = N.spgemm_work(A, B)
+    Wr = O.spgemm_work(hA, hB)
+    assert np.array_equal(Wd.cpu().numpy(), Wr)
+    qstar = int(Wr[-1])
+    P = N.esc_auto_partitions(qstar)
+    parts = N.partition_esc(A, B, Wd, qstar, P)
+    ref = O.esc_partition(hA, hB, P)
+    for f in ("query", "row", "col", "pos"):
+        assert np.array_equal(getattr(parts, f).cpu().numpy(), getattr(ref, f)), f
+    c_pos, c_crd, c_val, nnz_c = N.spgemm_esc(A, B, Wd, parts, qstar)
+    n = int(nnz_c.item())
+    r_pos, r_crd, r_val = O.spgemm(hA, hB)
+    assert n == len(r_crd)
+    assert np.array_equal(c_pos.cpu().numpy(), r_pos)
+    assert np.array_equal(c_crd[:n].cpu().numpy(), r_crd)
+    assert np.array_equal(c_val[:n].cpu().numpy(), r_val)
