@@ -319,7 +319,7 @@ nacho_status nacho_partition_esc(const nacho_matrix* A, const nacho_matrix* B, c
 
 /* nacho_spgemm_esc -- C = A B: expand (one CTA per partition writes the products [Q_p, Q_{p+1}) at
  * their expansion index: key (i, j), value A_ik * B_kj), stable radix sort by (i, j), contract (every
- * run of one (i, j) folded left to right, i.e. k ascending -- reading R22).  C stores (i, j) iff some
+ * run of one (i, j) folded left to right, i.e. k ascending -- reading R23).  C stores (i, j) iff some
  * product has that coordinate.  c_pos[A.nrows+1], c_crd / c_val capacity >= Q*; *nnz_c (device int64)
  * receives nnz(C).  The workspace holds the expansion twice (sort buffers) and the run indices. */
 size_t nacho_spgemm_esc_workspace_size(const nacho_matrix* A, const nacho_matrix* B, int64_t qstar);
@@ -327,7 +327,7 @@ nacho_status nacho_spgemm_esc(const nacho_matrix* A, const nacho_matrix* B, cons
                               int64_t qstar, int64_t* c_pos, int32_t* c_crd, void* c_val, int64_t* nnz_c, void* ws,
                               size_t ws_bytes, void* stream);
 
-/* nacho_sssmm_esc_count / nacho_sssmm_esc -- Z = S (.) (A B) (reading R23: Z_ij = S_ij * C_ij on the
+/* nacho_sssmm_esc_count / nacho_sssmm_esc -- Z = S (.) (A B) (reading R24: Z_ij = S_ij * C_ij on the
  * coordinates S and C both store).  The expansion over the same W / partition keeps the products whose
  * j is stored in S_i: count per partition -> part_off (device int64[P+1], exclusive prefix; part_off[P]
  * = kept products, which the caller reads) -> fill in expansion order -> sort -> contract.  Z

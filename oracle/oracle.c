@@ -937,7 +937,7 @@ static int cmp_i32(const void *a, const void *b) {
 /* C = A B, CSR x CSR -> CSR, with ESC's result: C stores (i, j) iff some k has A_ik and B_kj stored
  * (structurally, whatever the sum); the value is the left fold over k ascending (the order a stable
  * sort of T by (i, j) keeps) of the products A_ik * B_kj, each rounded in the value type, starting
- * from the first product (reading R22).  Row by row with a dense accumulator (Gustavson's order,
+ * from the first product (reading R23).  Row by row with a dense accumulator (Gustavson's order,
  * the same fold).  Returns nnz(C), or -1 (shape / capacity). */
 int64_t oracle_spgemm(const or_matrix *A, const or_matrix *B, int64_t *c_pos, int32_t *c_crd, void *c_val,
                       int64_t cap) {
@@ -983,7 +983,7 @@ int64_t oracle_spgemm(const or_matrix *A, const or_matrix *B, int64_t *c_pos, in
 }
 
 /* Sampled SpGEMM (SSSMM): Z = S (.) (A B).  Z stores (i, j) iff S stores it and C = A B
- * stores it structurally; Z_ij = S_ij * C_ij with C_ij the ESC fold of oracle_spgemm (reading R23:
+ * stores it structurally; Z_ij = S_ij * C_ij with C_ij the ESC fold of oracle_spgemm (reading R24:
  * the sampling restricts the expansion to j in S_i, which leaves the products of every kept (i, j)
  * and their order unchanged, and the sampled value scales the contracted sum).  Returns nnz(Z) or
  * -1. */

@@ -13,9 +13,9 @@
 //             the offsets are the queries themselves); SSSMM keeps the products whose j is stored
 //             in S_i (count per partition, exclusive scan, order-preserving fill);
 //   sort      a stable radix sort by key (CUB, a library primitive as SURVEY A24 / K6 allow) keeps
-//             the products of one (i, j) in expansion order, i.e. k ascending (reading R22);
+//             the products of one (i, j) in expansion order, i.e. k ascending (reading R23);
 //   contract  run heads -> exclusive scan -> one thread per run folds it left to right in the value
-//             type and writes C.crd / C.val / the row pointers (SSSMM: times S_ij, reading R23).
+//             type and writes C.crd / C.val / the row pointers (SSSMM: times S_ij, reading R24).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 

@@ -1,7 +1,7 @@
 """GPU parity of the ESC scatter kernels (nacho_spgemm_work, nacho_partition_esc, nacho_spgemm_esc,
 nacho_sssmm_esc_count / nacho_sssmm_esc) against the oracle, through the C ABI: the work prefix, every
 boundary field and the whole output (pos, crd, val) bit-exact -- the products and their k-ordered
-left fold are the same operations in the same order on both sides (reading R22 / R23)."""
+left fold are the same operations in the same order on both sides (reading R23 / R24)."""
 import numpy as np
 import pytest
 import torch

@@ -3,7 +3,7 @@ oracle_sssmm; P:2063-2074 expand-sort-contract, Listing 6's broadcast-scaled cos
 SSSMM P:2540-2559) against what the mathematics fixes: the dense product on small integers (exact)
 and in fp64, the structural (boolean) product, a different closed form of the expansion size,
 explicit enumeration of the expansion on tiny inputs, identities, a hand-worked example, and an fp32
-case whose value depends on the summation order (reading R22: left fold over k ascending)."""
+case whose value depends on the summation order (reading R23: left fold over k ascending)."""
 import numpy as np
 import pytest
 
