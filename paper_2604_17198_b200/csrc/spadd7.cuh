@@ -324,6 +324,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
           }
         }
       }
+      S7_T0();
       int32_t* zc = a.z_crd + off;
       V* zv = a.z_val + off;
       for (int q = lane; q < total; q += 32) {
@@ -332,6 +333,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
       }
       const int32_t* zrel = reinterpret_cast<const int32_t*>(g.pos);
       for (int l = lane + 1; l <= lrows; l += 32) a.z_pos[a0 + l] = off + zrel[l];
+      if (lane == 0) S7_ACC(8);   // emission: writing Z (dev builds)
     }
     fence_proxy_async();   // generic accesses of the stage before the producer's bulk copies
     __syncwarp();
