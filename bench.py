@@ -693,7 +693,8 @@ def bench_esc(N, W, torch, scale, K, Wu, timer, sampled=False):
         n = int(part_off[-1].item())
     else:
         n = qstar
-    need = N.lib.nacho_spgemm_esc_workspace_size(ctypes.byref(aa), ctypes.byref(ba), n)
+    need = (N.lib.nacho_sssmm_esc_workspace_size if sampled else N.lib.nacho_spgemm_esc_workspace_size)(
+        ctypes.byref(aa), ctypes.byref(ba), n)
     ws = torch.empty(need, dtype=torch.uint8, device="cuda")
     wws = torch.empty(max(1, N.lib.nacho_spgemm_work_workspace_size(ctypes.byref(aa))), dtype=torch.uint8, device="cuda")
     c_pos = torch.empty(M + 1, dtype=torch.int64, device="cuda")
