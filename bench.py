@@ -665,8 +665,11 @@ def bench_spmm(N, W, torch, scale, K, Wu, timer):
     times, sec = timer.run(step, K, Wu, ["partition", "spmm+fixup"])
     M, Nc, nnz, nb = A.nrows, A.ncols, A.nnz, wl.nb
     algo = nnz * 8 + (M + 1) * 8 + Nc * nb * 4 + M * nb * 4
+    # gather-granularity bound: one B row (nb * 4 bytes) per nonzero (B is 50x the L2, and 3/4 of the
+    # columns are uniform over it), plus A once and C once
+    gather = nnz * 8 + (M + 1) * 8 + nnz * nb * 4 + M * nb * 4
     return dict(work=nnz, times=times, sec=sec, algo_step=algo, kernel_bytes={"spmm+fixup": algo}, P=P, dtype="f32",
-                wl=wl)
+                wl=wl, gather_bytes=gather)
 
 
 def bench_esc(N, W, torch, scale, K, Wu, timer, sampled=False):

@@ -431,16 +431,18 @@ int64_t staged_chunks(int64_t max_work, int32_t k) {
 }
 
 struct StagedWs {   // carving of the staged workspace for nchunk chunks
-  int64_t* cnt; unsigned long long* blk; int64_t* prov; int64_t* rows; char* stage;
+  int64_t* cnt; unsigned long long* blk; int64_t* blk_off; int64_t* prov; int64_t* rows; char* stage;
 };
 size_t staged_ws_layout(int64_t nchunk, char* ws, StagedWs* out) {
   size_t o = 0;
   auto take = [&](size_t bytes) { const size_t at = o; o += align_up(bytes); return at; };
   const size_t c = take((size_t)(nchunk + 1) * 8), b = take((size_t)((nchunk >> kS4BlkShift) + 1) * 8),
+               bo = take((size_t)((nchunk >> kS4BlkShift) + 2) * 8),
                pv = take((size_t)nchunk * 8), r = take((size_t)nchunk * 16);
   if (out) {
     out->cnt = reinterpret_cast<int64_t*>(ws + c);
     out->blk = reinterpret_cast<unsigned long long*>(ws + b);
+    out->blk_off = reinterpret_cast<int64_t*>(ws + bo);
     out->prov = reinterpret_cast<int64_t*>(ws + pv);
     out->rows = reinterpret_cast<int64_t*>(ws + r);
     out->stage = ws + o;
@@ -462,7 +464,13 @@ nacho_status run_spadd_staged(const nacho_matrix* ops, int32_t k, const nacho_pa
   Spadd4Args<T> a{make_ops(ops, k), parts_arg(parts), w.cnt, part_off, nullptr, nullptr, z_pos, t_crd, t_val, w.blk,
                   (int32_t)chunks, w.prov, w.rows};
   NACHO_TRY((launch_spadd4<T, kS4Stage>(a, st, nchunk)));
+  // the block sums -> their exclusive prefix (one small scan: every placement CTA then reads one value
+  // instead of summing all preceding blocks, O(nchunk) instead of O(nchunk^2 / 512) loads)
+  const int64_t nblk = ((nchunk - 1) >> kS4BlkShift) + 1;
+  scan_counts_kernel<1024><<<1, 1024, 0, st>>>(reinterpret_cast<const int64_t*>(w.blk), nblk, w.blk_off);
+  NACHO_TRY(launched("scan_counts_kernel (block sums)"));
   Spadd4Args<T> c = a;
+  c.blk_cnt = reinterpret_cast<unsigned long long*>(w.blk_off);   // the placement reads the prefix
   c.z_crd = z_crd;
   c.z_val = z_val;
   s4_place_kernel<T><<<(unsigned)nchunk, kS4Threads, 0, st>>>(c, t_crd, t_val);

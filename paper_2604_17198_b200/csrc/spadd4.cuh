@@ -76,6 +76,7 @@ struct Spadd4Args {
   int32_t* z_crd;
   T* z_val;
   unsigned long long* blk_cnt;    // kS4Stage: union sizes summed per block of 2^kS4BlkShift chunks
+                                  // (placement: their exclusive prefix)
   int32_t chunks;                 // kS4Stage: CTAs (chunks) per partition; 1 unless partitions exceed a tile
   int64_t* ch_prov;               // kS4Stage: per chunk, provisional offset sum_o b.pos[o]
   int64_t* ch_row;                // kS4Stage: per chunk, [2*c] first row, [2*c+1] end row
@@ -979,8 +980,7 @@ __global__ void __launch_bounds__(kS4Threads, 6) s4_place_kernel(const __grid_co
   const int64_t nu = ldg(a.part_cnt + p), prov = ldg(a.ch_prov + p);
   const int64_t r0 = ldg(a.ch_row + 2 * p), r1 = ldg(a.ch_row + 2 * p + 1);
   const int64_t b = p >> kS4BlkShift;
-  unsigned long long v = 0;
-  for (int64_t i = tid; i < b; i += kS4Threads) v += a.blk_cnt[i];
+  unsigned long long v = tid == 0 ? a.blk_cnt[b] : 0ull;   // exclusive prefix of the block sums (run_spadd_staged)
   const int64_t q = (b << kS4BlkShift) + tid;
   if (q < p) v += (unsigned long long)ldg(a.part_cnt + q);
   constexpr int U = kS4Tile / kS4Threads;   // a chunk's union fits one round (nu <= kS4Tile)

@@ -205,8 +205,8 @@ constexpr int kSm2Groups = 32;       // 8-lane groups per CTA (256 threads)
 constexpr int kSm2Items = 32;        // positions per group
 constexpr int kSm2Tile = kSm2Groups * kSm2Items;
 #ifndef NACHO_SM2_BATCH   // nonzeros whose B rows a lane group loads before using them (registers: 8 per nonzero)
-#define NACHO_SM2_BATCH 4
-#define NACHO_SM2_MINB 3
+#define NACHO_SM2_BATCH 8  // C4: batch 8 / 2 CTAs per SM 65.0 ms, batch 4 / 3 CTAs 67.1, 4 / 4 72.1, 2 / 5 84.5
+#define NACHO_SM2_MINB 2
 #endif
 constexpr int kSm2Batch = NACHO_SM2_BATCH;
 

@@ -163,3 +163,15 @@ def test_esc_spgemm_bench_scale():
     assert np.array_equal(c_pos.cpu().numpy(), r_pos)
     assert np.array_equal(c_crd[:n].cpu().numpy(), r_crd)
     assert np.array_equal(c_val[:n].cpu().numpy(), r_val)
+
+
+def test_esc_sssmm_bench_scale():
+    """The ESC SSSMM line of bench.py at its own size (Z = C (.) (A B) on C2's operands, ~1e8 products
+    expanded, the sampled ones kept): Z bit-exact against the oracle."""
+    wl = W.build("c2", 1.0, device="cuda")
+    A, B, S = wl.ops
+    z_pos, z_crd, z_val = N.sssmm(S, A, B)
+    r_pos, r_crd, r_val = O.sssmm(S.numpy(), A.numpy(), B.numpy())
+    assert np.array_equal(z_pos.cpu().numpy(), r_pos)
+    assert np.array_equal(z_crd.cpu().numpy(), r_crd)
+    assert np.array_equal(z_val.cpu().numpy(), r_val)
