@@ -34,5 +34,16 @@ for dt in (np.float32, np.float64):
         N.spmv(B, x, N.partition([B], P) if P else None)
 Bm = torch.from_numpy(rng.uniform(0.5, 1.5, (1500, 64)).astype(np.float32)).to(dev)
 N.spmm(A.to(dev), Bm)
+# intersections (Hadamard, inner product) on the SpAdd operands
+parts = N.partition(dops, N.auto_partitions(dops, "spadd"))
+N.hadamard_k(dops, parts)
+N.inner_k(dops, parts)
+# ESC scatter kernels: SpGEMM (work, partition, expand, sort, contract) and sampled SpGEMM
+Ae = random_csr(rng, 200, 150, 0.03, dense_rows=[9]).to(dev)
+Be = random_csr(rng, 150, 170, 0.04, dense_rows=[2]).to(dev)
+Se = random_csr(rng, 200, 170, 0.1).to(dev)
+for P in (None, 7):
+    N.spgemm(Ae, Be, P=P)
+    N.sssmm(Se, Ae, Be, P=P)
 torch.cuda.synchronize()
 print("sanitize run done")
