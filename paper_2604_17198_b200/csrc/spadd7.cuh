@@ -49,7 +49,11 @@ struct S7Cfg {
 #else
   static constexpr int NS = sizeof(V) == 4 && K <= 3 ? 3 : 2;     // stages
 #endif
+#ifdef NACHO_S7_MINB   // tuning override
+  static constexpr int MINB = NACHO_S7_MINB;
+#else
   static constexpr int MINB = sizeof(V) == 4 && K <= 3 ? 3 : 2;   // CTAs / SM (64 registers at 3)
+#endif
 };
 
 template <typename V>
