@@ -342,7 +342,9 @@ nacho_status nacho_sssmm_esc(const nacho_matrix* S, const nacho_matrix* A, const
 
 /* ------------------------------------------------------------------------------------------------
  * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.
- * Synchronous on `stream` (it reads one flag back).  Returns NACHO_ERR_FORMAT on a violation. */
+ * Synchronous on `stream` (it reads one flag back).  Returns NACHO_ERR_FORMAT on a violation.  The one
+ * exception to "no device allocations": a 4-byte result flag, cudaMallocAsync'd and freed on `stream`
+ * inside the call. */
 nacho_status nacho_validate(const nacho_matrix* A, void* stream);
 
 /* ------------------------------------------------------------------------------------------------
