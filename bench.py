@@ -700,10 +700,12 @@ def bench_esc(N, W, torch, scale, K, Wu, timer, sampled=False):
     import ctypes
     if sampled:
         part_off = torch.empty(P + 1, dtype=torch.int64, device="cuda")
+        mask = torch.empty(N.lib.nacho_sssmm_mask_bytes(qstar, P), dtype=torch.uint8, device="cuda")
         cws = torch.empty(max(1, N.lib.nacho_sssmm_count_workspace_size(P)), dtype=torch.uint8, device="cuda")
         pc = parts.c()
         N._check(N.lib.nacho_sssmm_esc_count(ctypes.byref(sa), ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd),
-                                             ctypes.byref(pc), N._ptr(part_off), N._ptr(cws), cws.numel(), None))
+                                             ctypes.byref(pc), N._ptr(part_off), N._ptr(mask), N._ptr(cws),
+                                             cws.numel(), None))
         n = int(part_off[-1].item())
     else:
         n = qstar
@@ -728,11 +730,13 @@ def bench_esc(N, W, torch, scale, K, Wu, timer, sampled=False):
             m.append(ev(torch))
         if sampled:
             N._check(N.lib.nacho_sssmm_esc_count(ctypes.byref(sa), ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd),
-                                                 ctypes.byref(pc), N._ptr(part_off), N._ptr(cws), cws.numel(), None))
+                                                 ctypes.byref(pc), N._ptr(part_off), N._ptr(mask), N._ptr(cws),
+                                                 cws.numel(), None))
             if timed:
                 m.append(ev(torch))
             N._check(N.lib.nacho_sssmm_esc(ctypes.byref(sa), ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd),
-                                           ctypes.byref(pc), N._ptr(part_off), n, N._ptr(c_pos), N._ptr(c_crd),
+                                           ctypes.byref(pc), N._ptr(part_off), N._ptr(mask), n, N._ptr(c_pos),
+                                           N._ptr(c_crd),
                                            N._ptr(c_val), N._ptr(nnz_c), N._ptr(ws), need, None))
         else:
             N._check(N.lib.nacho_spgemm_esc(ctypes.byref(aa), ctypes.byref(ba), N._ptr(Wd), ctypes.byref(pc), qstar,

@@ -331,14 +331,19 @@ nacho_status nacho_spgemm_esc(const nacho_matrix* A, const nacho_matrix* B, cons
  * coordinates S and C both store).  The expansion over the same W / partition keeps the products whose
  * j is stored in S_i: count per partition -> part_off (device int64[P+1], exclusive prefix; part_off[P]
  * = kept products, which the caller reads) -> fill in expansion order -> sort -> contract.  Z
- * capacity >= part_off[P]. */
+ * capacity >= part_off[P].  keep_mask (device, nacho_sssmm_mask_bytes(Q*, P) bytes, caller-owned) carries
+ * the count pass's membership bits to the fill (the assembly records the predicate, the compute reuses
+ * it: no second search in S). */
+size_t nacho_sssmm_mask_bytes(int64_t qstar, int32_t P);
 size_t nacho_sssmm_count_workspace_size(int32_t P);
 nacho_status nacho_sssmm_esc_count(const nacho_matrix* S, const nacho_matrix* A, const nacho_matrix* B, const int64_t* W,
-                                   const nacho_parts* parts, int64_t* part_off, void* ws, size_t ws_bytes, void* stream);
+                                   const nacho_parts* parts, int64_t* part_off, uint8_t* keep_mask, void* ws,
+                                   size_t ws_bytes, void* stream);
 size_t nacho_sssmm_esc_workspace_size(const nacho_matrix* A, const nacho_matrix* B, int64_t n_kept);
 nacho_status nacho_sssmm_esc(const nacho_matrix* S, const nacho_matrix* A, const nacho_matrix* B, const int64_t* W,
-                             const nacho_parts* parts, const int64_t* part_off, int64_t n_kept, int64_t* z_pos,
-                             int32_t* z_crd, void* z_val, int64_t* nnz_z, void* ws, size_t ws_bytes, void* stream);
+                             const nacho_parts* parts, const int64_t* part_off, const uint8_t* keep_mask, int64_t n_kept,
+                             int64_t* z_pos, int32_t* z_crd, void* z_val, int64_t* nnz_z, void* ws, size_t ws_bytes,
+                             void* stream);
 
 /* ------------------------------------------------------------------------------------------------
  * nacho_validate -- full structural check of an operand (sorted levels; R10) on the device.

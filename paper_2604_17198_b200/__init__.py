@@ -106,10 +106,12 @@ def _load():
     L.nacho_spgemm_esc.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]
     L.nacho_sssmm_count_workspace_size.argtypes = [i32]
     L.nacho_sssmm_count_workspace_size.restype = sz
-    L.nacho_sssmm_esc_count.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_sssmm_mask_bytes.argtypes = [i64, i32]
+    L.nacho_sssmm_mask_bytes.restype = sz
+    L.nacho_sssmm_esc_count.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     L.nacho_sssmm_esc_workspace_size.argtypes = [vp, vp, i64]
     L.nacho_sssmm_esc_workspace_size.restype = sz
-    L.nacho_sssmm_esc.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]
+    L.nacho_sssmm_esc.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]
     # multi-GPU (dist.cuh)
     L.nacho_dist_unique_id_size.restype = sz
     L.nacho_dist_unique_id.argtypes = [vp]
@@ -140,7 +142,7 @@ EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", 
            "nacho_partition_csf", "nacho_csf_spadd_k_workspace_size", "nacho_csf_spadd_k",
            "nacho_spgemm_work_workspace_size", "nacho_spgemm_work", "nacho_esc_auto_partitions",
            "nacho_partition_esc", "nacho_spgemm_esc_workspace_size", "nacho_spgemm_esc",
-           "nacho_sssmm_count_workspace_size", "nacho_sssmm_esc_count", "nacho_sssmm_esc_workspace_size",
+           "nacho_sssmm_mask_bytes", "nacho_sssmm_count_workspace_size", "nacho_sssmm_esc_count", "nacho_sssmm_esc_workspace_size",
            "nacho_sssmm_esc",
            "nacho_dist_unique_id_size", "nacho_dist_unique_id", "nacho_dist_init",
            "nacho_dist_destroy", "nacho_dist_broadcast", "nacho_device_cuts", "nacho_shard_rows", "nacho_dist_seam",
@@ -600,11 +602,12 @@ def sssmm(S, A, B, P: int = None, stream=None):
     P = P or esc_auto_partitions(qstar)
     parts = partition_esc(A, B, W, qstar, P, stream=stream)
     part_off = torch.empty(P + 1, dtype=torch.int64, device=dev)
+    mask = torch.empty(lib.nacho_sssmm_mask_bytes(qstar, P), dtype=torch.uint8, device=dev)
     need = lib.nacho_sssmm_count_workspace_size(P)
     ws, _ = _workspace(need, dev)
     pc = parts.c()
     _check(lib.nacho_sssmm_esc_count(ctypes.byref(s), ctypes.byref(a), ctypes.byref(b), _ptr(W), ctypes.byref(pc),
-                                     _ptr(part_off), _ptr(ws), need, _stream(stream)))
+                                     _ptr(part_off), _ptr(mask), _ptr(ws), need, _stream(stream)))
     n_kept = int(part_off[-1].item())
     z_pos = torch.empty(A.nrows + 1, dtype=torch.int64, device=dev)
     z_crd = torch.empty(max(n_kept, 1), dtype=torch.int32, device=dev)
@@ -613,8 +616,8 @@ def sssmm(S, A, B, P: int = None, stream=None):
     need = lib.nacho_sssmm_esc_workspace_size(ctypes.byref(a), ctypes.byref(b), n_kept)
     ws, _ = _workspace(need, dev)
     _check(lib.nacho_sssmm_esc(ctypes.byref(s), ctypes.byref(a), ctypes.byref(b), _ptr(W), ctypes.byref(pc),
-                               _ptr(part_off), n_kept, _ptr(z_pos), _ptr(z_crd), _ptr(z_val), _ptr(nnz_z), _ptr(ws),
-                               need, _stream(stream)))
+                               _ptr(part_off), _ptr(mask), n_kept, _ptr(z_pos), _ptr(z_crd), _ptr(z_val), _ptr(nnz_z),
+                               _ptr(ws), need, _stream(stream)))
     n = int(nnz_z.item())
     return z_pos, z_crd[:n], z_val[:n]
 

@@ -101,7 +101,12 @@ struct EscExpandArgs {
   int64_t* cnt;             // kEscCount: [P]; kEscFill: part_off [P + 1]
   unsigned long long* key;  // kEscAll / kEscFill
   V* val;
+  uint8_t* mask;            // SSSMM: the count pass's keep bits (8 products per byte), read by the fill
 };
+
+// Byte offset of partition p's keep bits in the SSSMM mask (floor(Q_p / 8) + p: monotone, and
+// partition p's ceil((Q_{p+1} - Q_p) / 8) bytes never reach partition p + 1's).
+__device__ __forceinline__ int64_t esc_mask_base(int64_t Qp, int64_t p) { return (Qp >> 3) + p; }
 
 // One CTA per partition, in chunks of kEscChunk products: thread t walks products
 // [c0 + 8t, c0 + 8t + 8) sequentially -- one search for the first product's A entry q and row i,
@@ -170,7 +175,9 @@ __global__ void __launch_bounds__(kEscThreads) esc_expand_kernel(const EscExpand
           const int64_t r = bs + (w - wq);
           const int32_t j = ldg(o.b_crd + r);
           bool kp = true;
-          if (MODE != kEscAll) {   // sampled: is j stored in S_i?  (j rises along B's row: gallop)
+          if (MODE == kEscFill) {   // sampled: the count pass recorded the membership
+            kp = (a.mask[esc_mask_base(Q0, p) + ((wb - Q0) >> 3)] >> v) & 1u;
+          } else if (MODE != kEscAll) {   // sampled: is j stored in S_i?  (j rises along B's row: gallop)
             if (fresh) {
               sp = ldg(o.s_pos + i);
               se = ldg(o.s_pos + i + 1);
@@ -198,6 +205,7 @@ __global__ void __launch_bounds__(kEscThreads) esc_expand_kernel(const EscExpand
         }
       }
     }
+    if (MODE == kEscCount && wb < we) a.mask[esc_mask_base(Q0, p) + ((wb - Q0) >> 3)] = (uint8_t)keep;
     const int n_chunk = (int)min((int64_t)kEscChunk, Q1 - c0);
     if (MODE == kEscAll) {   // every product at its expansion index
 #pragma unroll
@@ -513,6 +521,8 @@ static nacho_status check_sample(const nacho_matrix* S, const nacho_matrix* A, c
   return NACHO_SUCCESS;
 }
 
+size_t nacho_sssmm_mask_bytes(int64_t qstar, int32_t P) { return (size_t)(qstar > 0 ? qstar : 0) / 8 + (size_t)P + 2; }
+
 size_t nacho_sssmm_count_workspace_size(int32_t P) {
   size_t t = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, t, (const int64_t*)nullptr, (int64_t*)nullptr, (int64_t)P + 1);
@@ -520,20 +530,21 @@ size_t nacho_sssmm_count_workspace_size(int32_t P) {
 }
 
 nacho_status nacho_sssmm_esc_count(const nacho_matrix* S, const nacho_matrix* A, const nacho_matrix* B, const int64_t* W,
-                                   const nacho_parts* parts, int64_t* part_off, void* ws, size_t ws_bytes, void* stream) {
+                                   const nacho_parts* parts, int64_t* part_off, uint8_t* keep_mask, void* ws,
+                                   size_t ws_bytes, void* stream) {
   ESC_TRY(check_sample(S, A, B));
   ESC_TRY(check_esc_parts(parts));
-  if (!W || !part_off) return efail(NACHO_ERR_INVALID_ARG, "null W / part_off");
+  if (!W || !part_off || !keep_mask) return efail(NACHO_ERR_INVALID_ARG, "null W / part_off / keep_mask");
   const size_t need = nacho_sssmm_count_workspace_size(parts->P);
   if (!ws || ws_bytes < need) return efail(NACHO_ERR_WORKSPACE, "nacho_sssmm_esc_count: workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const EscOps o = make_esc(A, B, S, W);
   if (cudaMemsetAsync(part_off + parts->P, 0, 8, st) != cudaSuccess) return efail(NACHO_ERR_CUDA, "memset");
   if (A->dtype == NACHO_F64) {
-    EscExpandArgs<double> ea{o, esc_parts(parts), part_off, nullptr, nullptr};
+    EscExpandArgs<double> ea{o, esc_parts(parts), part_off, nullptr, nullptr, keep_mask};
     esc_expand_kernel<double, kEscCount><<<parts->P, kEscThreads, 0, st>>>(ea);
   } else {
-    EscExpandArgs<float> ea{o, esc_parts(parts), part_off, nullptr, nullptr};
+    EscExpandArgs<float> ea{o, esc_parts(parts), part_off, nullptr, nullptr, keep_mask};
     esc_expand_kernel<float, kEscCount><<<parts->P, kEscThreads, 0, st>>>(ea);
   }
   ESC_TRY(nacho_internal_launched("esc_expand_kernel (count)"));
@@ -548,11 +559,12 @@ size_t nacho_sssmm_esc_workspace_size(const nacho_matrix* A, const nacho_matrix*
 }
 
 nacho_status nacho_sssmm_esc(const nacho_matrix* S, const nacho_matrix* A, const nacho_matrix* B, const int64_t* W,
-                             const nacho_parts* parts, const int64_t* part_off, int64_t n_kept, int64_t* z_pos,
-                             int32_t* z_crd, void* z_val, int64_t* nnz_z, void* ws, size_t ws_bytes, void* stream) {
+                             const nacho_parts* parts, const int64_t* part_off, const uint8_t* keep_mask, int64_t n_kept,
+                             int64_t* z_pos, int32_t* z_crd, void* z_val, int64_t* nnz_z, void* ws, size_t ws_bytes,
+                             void* stream) {
   ESC_TRY(check_sample(S, A, B));
   ESC_TRY(check_esc_parts(parts));
-  if (!W || !part_off || !z_pos || !nnz_z || n_kept < 0 || (n_kept > 0 && (!z_crd || !z_val)))
+  if (!W || !part_off || !keep_mask || !z_pos || !nnz_z || n_kept < 0 || (n_kept > 0 && (!z_crd || !z_val)))
     return efail(NACHO_ERR_INVALID_ARG, "null argument");
   const size_t need = nacho_sssmm_esc_workspace_size(A, B, n_kept);
   if (!ws || ws_bytes < need) return efail(NACHO_ERR_WORKSPACE, "nacho_sssmm_esc: workspace too small");
@@ -563,7 +575,8 @@ nacho_status nacho_sssmm_esc(const nacho_matrix* S, const nacho_matrix* A, const
   const size_t nn = (size_t)(n_kept > 0 ? n_kept : 1);
   if (A->dtype == NACHO_F64) {
     EscExpandArgs<double> ea{o, esc_parts(parts), const_cast<int64_t*>(part_off),
-                             reinterpret_cast<unsigned long long*>(w8), reinterpret_cast<double*>(w8 + 2 * al(nn * 8))};
+                             reinterpret_cast<unsigned long long*>(w8), reinterpret_cast<double*>(w8 + 2 * al(nn * 8)),
+                             const_cast<uint8_t*>(keep_mask)};
     if (n_kept > 0) {
       esc_expand_kernel<double, kEscFill><<<parts->P, kEscThreads, 0, st>>>(ea);
       ESC_TRY(nacho_internal_launched("esc_expand_kernel (fill)"));
@@ -571,7 +584,7 @@ nacho_status nacho_sssmm_esc(const nacho_matrix* S, const nacho_matrix* A, const
     return sort_contract<double, true>(o, n_kept, eb, w8, z_pos, z_crd, static_cast<double*>(z_val), nnz_z, st);
   }
   EscExpandArgs<float> ea{o, esc_parts(parts), const_cast<int64_t*>(part_off), reinterpret_cast<unsigned long long*>(w8),
-                          reinterpret_cast<float*>(w8 + 2 * al(nn * 8))};
+                          reinterpret_cast<float*>(w8 + 2 * al(nn * 8)), const_cast<uint8_t*>(keep_mask)};
   if (n_kept > 0) {
     esc_expand_kernel<float, kEscFill><<<parts->P, kEscThreads, 0, st>>>(ea);
     ESC_TRY(nacho_internal_launched("esc_expand_kernel (fill)"));
