@@ -104,6 +104,9 @@ nacho_status nacho_partition_slice(const nacho_matrix* ops, int32_t k, int32_t P
 /* Partition count the kernels below pick when the caller does not fix P: ceil(Q* / tile), tile being
  * the per-CTA work of the kernel for that operation (op: 0 spmv, 1 spadd, 2 spmm). */
 int32_t nacho_auto_partitions(const nacho_matrix* ops, int32_t k, int32_t op);
+/* The largest partition (entries summed over the k operands) the single-read SpAdd / intersection
+ * kernels take: a stage of 256 x 8 slots minus the bulk-copy pads (7 per operand); 0 for a bad k. */
+int32_t nacho_spadd_tile(int32_t k);
 
 /* ------------------------------------------------------------------------------------------------
  * nacho_spmv -- y = A x over a partition of A (SpMV is the broadcast example of P:1742-1744; the

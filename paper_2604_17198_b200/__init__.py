@@ -59,6 +59,8 @@ def _load():
     L.nacho_partition_slice.argtypes = [vp, i32, i32, i32, vp, vp]
     L.nacho_auto_partitions.argtypes = [vp, i32, i32]
     L.nacho_auto_partitions.restype = i32
+    L.nacho_spadd_tile.argtypes = [i32]
+    L.nacho_spadd_tile.restype = i32
     L.nacho_spmv_workspace_size.argtypes = [vp, i32]
     L.nacho_spmv_workspace_size.restype = sz
     L.nacho_spmv.argtypes = [vp, vp, vp, vp, i32, vp, sz, vp]
@@ -132,7 +134,7 @@ def _load():
 
 lib = _load()
 
-EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", "nacho_spmv_workspace_size", "nacho_spmv",
+EXPORTS = ["nacho_partition", "nacho_partition_slice", "nacho_auto_partitions", "nacho_spadd_tile", "nacho_spmv_workspace_size", "nacho_spmv",
            "nacho_spadd_k_workspace_size", "nacho_spadd_k_count", "nacho_spadd_k_fill", "nacho_spadd_k",
            "nacho_spadd_k_staged_workspace_size", "nacho_spadd_k_staged",
            "nacho_spmm_workspace_size", "nacho_spmm", "nacho_validate", "nacho_last_error",

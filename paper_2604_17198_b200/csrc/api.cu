@@ -1190,6 +1190,8 @@ nacho_status nacho_partition_slice(const nacho_matrix* ops, int32_t k, int32_t P
   return launch_partition(ops, k, parts_arg(out), static_cast<cudaStream_t>(stream), P, p_begin);
 }
 
+int32_t nacho_spadd_tile(int32_t k) { return k < 1 || k > NACHO_MAX_K ? 0 : s5_max_entries(k); }
+
 int32_t nacho_auto_partitions(const nacho_matrix* ops, int32_t k, int32_t op) {
   if (!ops || k < 1) return 1;
   const int64_t work = total_cost(ops, k);

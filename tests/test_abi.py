@@ -51,8 +51,9 @@ def test_auto_partitions_and_workspace_host_only():
         m = _desc(nnz, dt)
         assert L.nacho_auto_partitions(ctypes.byref(m), 1, 0) == max(1, -(-nnz // tile))
     ops = (N.Matrix * 3)(*[_desc(10**7) for _ in range(3)])
-    # SpAdd: a 2048-slot stage minus the bulk-copy pad (7 per operand) and Theorem 1's slack k - 1
-    assert L.nacho_auto_partitions(ops, 3, 1) == -(-3 * 10**7 // (2048 - 7 * 3 - 2))
+    # SpAdd: a 256 x 8-slot stage minus the bulk-copy pad (7 per operand) and Theorem 1's slack k - 1
+    assert L.nacho_spadd_tile(3) == 256 * 8 - 7 * 3 and L.nacho_spadd_tile(0) == 0
+    assert L.nacho_auto_partitions(ops, 3, 1) == -(-3 * 10**7 // (256 * 8 - 7 * 3 - 2))
     assert L.nacho_auto_partitions(ctypes.byref(_desc(10**6)), 1, 2) == -(-10**6 // 1024)
     m = _desc(10**6)
     assert L.nacho_spmv_workspace_size(ctypes.byref(m), 10) >= 10 * 12

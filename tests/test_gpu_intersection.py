@@ -27,7 +27,7 @@ def _ops(rng, k, M, Nc, dens, dtype=np.float32, dense_rows=()):
 def _check(ops, P=None, tol=None):
     dops = [A.to(DEV) for A in ops]
     k = len(ops)
-    if P and -(-sum(A.nnz for A in ops) // P) + k - 1 > 2048 - 7 * k:
+    if P and -(-sum(A.nnz for A in ops) // P) + k - 1 > N.lib.nacho_spadd_tile(k):
         parts = N.partition(dops, P)   # partitions larger than a stage: rejected, never overrun
         with pytest.raises(N.NachoError):
             N.hadamard_k(dops, parts)
@@ -59,7 +59,7 @@ def test_intersection_random(k):
         ops = _ops(rng, k, M, Nc, float(rng.uniform(0.001, 0.02)),
                    dense_rows=[int(rng.integers(M))] if trial % 2 == 0 else ())
         for P in (None, 7, 301):
-            if -(-sum(A.nnz for A in ops) // P if P else 0) + k > 2048 - 7 * k:
+            if -(-sum(A.nnz for A in ops) // P if P else 0) + k > N.lib.nacho_spadd_tile(k):
                 continue   # partitions must fit the stage
             _check(ops, P)
 

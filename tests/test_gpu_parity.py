@@ -222,7 +222,7 @@ def _spadd_check(ops, P=None):
     assert np.array_equal(sz_val[:n].cpu().numpy().view(np.uint8), rv.view(np.uint8)), "staged Z.val bits"
     # single-pass (look-back) variant, when the partitions fit its tile
     qstar = sum(A.nnz for A in ops)
-    if -(-qstar // parts.P) + len(ops) - 1 <= 2048:
+    if -(-qstar // parts.P) + len(ops) - 1 <= N.lib.nacho_spadd_tile(len(ops)):
         po = torch.full((parts.P + 1,), -1, dtype=torch.int64, device=DEV)
         fz_pos, fz_crd, fz_val = N.spadd_k_fused(dops, parts, part_off=po)
         n = int(fz_pos[-1].item())
