@@ -179,6 +179,9 @@ __device__ __forceinline__ void s5_merge_stage(const uint32_t* X, const uint16_t
 
 // ------------------------------------------------------------------ decoupled look-back
 constexpr unsigned long long kS5Agg = 1ull << 62, kS5Incl = 2ull << 62, kS5Val = (1ull << 62) - 1;
+#ifndef NACHO_LB_SLEEP_MAX   // look-back polling back-off cap (ns)
+#define NACHO_LB_SLEEP_MAX 256
+#endif
 
 // Warp 0: exclusive prefix of the counts of tiles < t, after the aggregate of t was published.
 __device__ __forceinline__ int64_t s5_lookback(unsigned long long* st, int64_t t) {
@@ -196,7 +199,7 @@ __device__ __forceinline__ int64_t s5_lookback(unsigned long long* st, int64_t t
       first = incl ? __ffs(incl) - 1 : 32;   // nearest predecessor with an inclusive prefix
       const unsigned need = first >= 31 ? kFull : ((2u << first) - 1);
       if ((ready & need) == need) break;
-      if ((v >> 62) == 0) { __nanosleep(ns); ns = ns < 256 ? 2 * ns : ns; v = ld_acquire(st + q); }
+      if ((v >> 62) == 0) { __nanosleep(ns); ns = ns < NACHO_LB_SLEEP_MAX ? 2 * ns : ns; v = ld_acquire(st + q); }
     }
     unsigned long long s = lane <= first ? (v & kS5Val) : 0ull;
 #pragma unroll

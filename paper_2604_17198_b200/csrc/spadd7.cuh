@@ -121,6 +121,12 @@ __device__ __forceinline__ void s7_wait(uint64_t* bar, uint32_t parity) {
 
 // Waits of the producer / emission warps: back off between polls so that a warp running ahead of
 // the compute warps does not take their issue slots.
+#ifndef NACHO_S7_SLEEP_P   // back-off of the waits (ns): producer (free stage), emission (loaded / computed
+#define NACHO_S7_SLEEP_P 256  // stage), compute warps (loaded stage)
+#define NACHO_S7_SLEEP_EF 64
+#define NACHO_S7_SLEEP_ED 256
+#define NACHO_S7_SLEEP_C 128
+#endif
 __device__ __forceinline__ void s7_wait_sleep(uint64_t* bar, uint32_t parity, unsigned ns) {
   while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
 }
@@ -156,7 +162,7 @@ __device__ __forceinline__ void s7_produce(const S7Args<V>& a, S7Smem<V, K>& sh)
     ++njob;
     {
       S7_T0();
-      s7_wait_sleep(&sh.empty[s], ph ^ 1u, 256);
+      s7_wait_sleep(&sh.empty[s], ph ^ 1u, NACHO_S7_SLEEP_P);
       if (lane == 0) S7_ACC(0);   // producer: waiting for a free stage
     }
     S7Stage<V, K>& g = sh.st[s];
@@ -290,7 +296,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
     const uint32_t ph = (uint32_t)(njob / NS) & 1u;
     // the look-back of a one-pass job runs while the compute warps merge it: it needs only the
     // predecessors' states, so it starts as soon as the job record is in the stage
-    s7_wait_sleep(&sh.full[s], ph, 64);
+    s7_wait_sleep(&sh.full[s], ph, NACHO_S7_SLEEP_EF);
     S7Stage<V, K>& g = sh.st[s];
     const int64_t t = g.tile;
     const int mode = g.mode;
@@ -307,7 +313,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
     }
     {
       S7_T0();
-      s7_wait_sleep(&sh.done[s], ph, 256);
+      s7_wait_sleep(&sh.done[s], ph, NACHO_S7_SLEEP_ED);
       if (lane == 0) S7_ACC(1);   // emission: waiting for a computed stage
     }
     if (lane == 0) sh.excl_ok[s] = 0;
@@ -468,7 +474,7 @@ __device__ __forceinline__ void s7_compute(const S7Args<V>& a, S7Smem<V, K>& sh)
     const int s = njob % NS;
     {
       S7_T0();
-      s7_wait_sleep(&sh.full[s], (uint32_t)(njob / NS) & 1u, 128);
+      s7_wait_sleep(&sh.full[s], (uint32_t)(njob / NS) & 1u, NACHO_S7_SLEEP_C);
       if (tid == 0) S7_ACC(3);   // compute: waiting for a loaded stage
     }
     S7Stage<V, K>& g = sh.st[s];
