@@ -190,14 +190,16 @@ __device__ __forceinline__ void warp_kway_select_t(const int32_t* const (&cp)[KM
     I Lo[KM], Uo[KM];
 #pragma unroll
     for (int o = 0; o < KM; ++o) {
-      if (o < k) {
+      Lo[o] = Uo[o] = 0;
+      if (o < k && o != m) {   // (the candidates' own window m brackets itself: no rank search)
         const I len = hi[o] - lo[o];
         const int j = lanes_less(u[o], cand, len > 0 ? 32 : 0);
         const I sjm = __shfl_sync(kFull, sp[o], j > 0 ? j - 1 : 0);
         const I sj = __shfl_sync(kFull, sp[o], j < 32 ? j : 31);
         Lo[o] = j > 0 ? sjm - lo[o] + 1 : 0;
         Uo[o] = j < 32 ? sj - lo[o] : len;
-        if (o != m) { L += Lo[o]; U += Uo[o]; }
+        L += Lo[o];
+        U += Uo[o];
       }
     }
     const unsigned below = __ballot_sync(kFull, U <= R);   // candidates <= v*
