@@ -230,20 +230,21 @@ __device__ __forceinline__ void warp_kway_select_t(const int32_t* const (&cp)[KM
   // entries of lower operands with a column <= it, of higher operands with a column < it, and the l
   // entries before it in its own window -- unique ranks, so exactly one entry has rank R
   int32_t vstar = INF;
+  bool found = false;   // warp-uniform: the one entry of rank R is found, the other windows are skipped
 #pragma unroll
   for (int o = 0; o < KM; ++o) {
-    if (o < k) {
+    if (o < k && !found && hi[o] > lo[o]) {
       const int32_t x = e[o];
       int rank = lane;
 #pragma unroll
       for (int o2 = 0; o2 < KM; ++o2) {
-        if (o2 < k && o2 != o) {
+        if (o2 < k && o2 != o && hi[o2] > lo[o2]) {
           const int n2 = (int)(hi[o2] - lo[o2]);
           rank += lanes_less(e[o2], (o2 < o && x != INF) ? x + 1 : x, n2);
         }
       }
       const unsigned hm = __ballot_sync(kFull, x != INF && (I)rank == R);
-      if (hm) vstar = __shfl_sync(kFull, x, __ffs(hm) - 1);
+      if (hm) { vstar = __shfl_sync(kFull, x, __ffs(hm) - 1); found = true; }
     }
   }
   col = vstar;
