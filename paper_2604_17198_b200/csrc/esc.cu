@@ -116,8 +116,13 @@ __device__ __forceinline__ int64_t esc_mask_base(int64_t Qp, int64_t p) { return
 constexpr int kEscVT = 8;
 constexpr int kEscChunk = kEscThreads * kEscVT;
 
+// CTAs per SM the registers are sized for (pinned: left free, ptxas picked 47-55 registers for the
+// count pass from one build to the next, 1.1-1.5 ms)
+template <int MODE>
+constexpr int esc_minb() { return MODE == kEscCount ? 5 : 3; }
+
 template <typename V, int MODE>
-__global__ void __launch_bounds__(kEscThreads) esc_expand_kernel(const EscExpandArgs<V> a) {
+__global__ void __launch_bounds__(kEscThreads, esc_minb<MODE>()) esc_expand_kernel(const EscExpandArgs<V> a) {
   __shared__ unsigned long long skey[MODE == kEscCount ? 1 : kEscChunk];
   __shared__ V sval[MODE == kEscCount ? 1 : kEscChunk];
   __shared__ int32_t wsum[kEscThreads / 32 + 1];
