@@ -29,21 +29,23 @@ def build_nacho(force=False, verbose=False):
     out = os.path.join(HERE, "libnacho.so")
     srcs = _sources(os.path.join(HERE, "csrc")) + [os.path.join(ROOT, "include", "nacho.h")]
     if force or _newer(out, srcs):
-        # one object per translation unit, then one link: compiling both .cu files in one nvcc call
-        # left the CUB sort kernels of esc.cu with run-to-run different register allocations (80 vs
-        # 90-105 registers, a 25 % slower sort); per-file compiles are reproducible
+        # one object per translation unit, then one link, and no --split-compile: split device
+        # compilation (and one nvcc call for both files) gave run-to-run different code for the same
+        # source -- spadd7 and the CUB sort kernels each came out in a fast and a slow variant (C2 step
+        # 0.3155 vs 0.3255 ms, SpGEMM 6.3 vs 8.0 ms); whole-unit compiles are reproducible (identical
+        # SASS) and are the fast variant.  The two units compile in parallel.
         base = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "-I", os.path.join(ROOT, "include")]
         if verbose:
             base.insert(1, "-Xptxas=-v")
-        objs = []
-        for name, split in (("api", True), ("esc", False)):
+        objs, procs = [], []
+        for name in ("api", "esc"):
             obj = os.path.join(HERE, f"{name}.o")
-            cmd = base + ["-c", os.path.join(HERE, "csrc", f"{name}.cu"), "-o", obj]
-            if split:   # device code of the big unit optimised in parallel
-                cmd.insert(1, f"--split-compile={max(1, min(16, os.cpu_count() or 1))}")
-            subprocess.check_call(cmd)
+            procs.append(subprocess.Popen(base + ["-c", os.path.join(HERE, "csrc", f"{name}.cu"), "-o", obj]))
             objs.append(obj)
+        for pr in procs:
+            if pr.wait() != 0:
+                raise subprocess.CalledProcessError(pr.returncode, pr.args)
         subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs])
         for obj in objs:
             os.remove(obj)
