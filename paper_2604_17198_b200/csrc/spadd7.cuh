@@ -337,6 +337,7 @@ __device__ __forceinline__ void s7_emit(const S7Args<V>& a, S7Smem<V, K>& sh) {
       S7_T0();
       int32_t* zc = a.z_crd + off;
       V* zv = a.z_val + off;
+#pragma unroll 4
       for (int q = lane; q < total; q += 32) {
         zc[q] = (int32_t)g.key[q];
         zv[q] = g.val[q];
